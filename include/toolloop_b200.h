@@ -1,0 +1,196 @@
+/*
+ * toolloop-b200 — C ABI of the B200-native GRPO trajectory-to-loss hot path.
+ *
+ * Drop-in boundary for the reference's Python operators (paths relative to
+ * /root/reference/pkg/src/toolloop/).  Every entry point:
+ *   - takes plain device pointers + sizes and a cudaStream_t (as void*),
+ *   - is stream-ordered and never synchronises the device,
+ *   - never allocates device memory: scratch comes from a caller-owned
+ *     workspace sized by the matching *_workspace_bytes() query,
+ *   - returns TL_OK (0) or a tl_status; tl_last_error() has the message.
+ * Length / shape validation that the reference performs eagerly
+ * (MaskMismatch, GroupTooSmall, ValueError) is done by the host caller on
+ * host-side metadata before launch; the codes below carry the same meaning.
+ *
+ * Data types: token ids int32, masks uint8, bf16 tensors as uint16_t bit
+ * patterns, log-probs float (perf mode) or double (parity mode).
+ */
+#ifndef TOOLLOOP_B200_H
+#define TOOLLOOP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TL_ABI_VERSION 1
+
+typedef void* tl_stream_t; /* cudaStream_t */
+
+typedef enum tl_status {
+  TL_OK = 0,
+  TL_ERR_INVALID_ARG = 1,     /* ValueError (config.py:70-78, loss.py:58-64)   */
+  TL_ERR_MASK_MISMATCH = 2,   /* errors.MaskMismatch  (errors.py:28)           */
+  TL_ERR_GROUP_TOO_SMALL = 3, /* errors.GroupTooSmall (errors.py:32)           */
+  TL_ERR_CUDA = 4,
+  TL_ERR_UNSUPPORTED = 5,
+  TL_ERR_WORKSPACE = 6
+} tl_status;
+
+const char* tl_last_error(void);
+int tl_abi_version(void);
+/* Number of kernels this library has launched since load (monotonic). */
+int64_t tl_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * K1 — trajectory packer.
+ * Replaces trajectory.flatten (trajectory.py:154-159), trajectory.action_mask
+ * (trajectory.py:162-167) and the per-token zip of rl.loss.token_records
+ * (loss.py:76-100), batched over all trajectories of a step.
+ *
+ * Segment table: segments are listed in trajectory order; trajectory b owns
+ * segments [traj_seg_off[b], traj_seg_off[b+1]).  Segment s has seg_len[s]
+ * token ids stored at token_pool[seg_src_off[s] ...] (any order in the pool,
+ * e.g. the arrival order of asynchronous rollout turns) and seg_is_action[s]
+ * = 1 for Segment.origin == "action".
+ * Outputs (varlen, packed order, T = n_tokens, A = action tokens):
+ *   input_ids[T], loss_mask[T], position_ids[T] (per-trajectory iota),
+ *   traj_of_token[T], cu_seqlens[B+1], act_off[B+1], act_idx[A].
+ * ---------------------------------------------------------------------- */
+size_t tl_pack_workspace_bytes(int32_t n_traj, int32_t n_seg);
+int tl_pack_varlen(const int32_t* token_pool, const int32_t* seg_src_off, const int32_t* seg_len,
+                   const uint8_t* seg_is_action, const int32_t* traj_seg_off, int32_t n_traj,
+                   int32_t n_seg, int64_t n_tokens, int32_t* input_ids, uint8_t* loss_mask,
+                   int32_t* position_ids, int32_t* traj_of_token, int32_t* cu_seqlens,
+                   int32_t* act_off, int32_t* act_idx, void* workspace, size_t workspace_bytes,
+                   tl_stream_t stream);
+/* Padded [B, lmax] view of a varlen pack: pad slots get pad_id / mask 0 /
+ * position 0.  Trajectories longer than lmax are an error (checked on host). */
+int tl_pack_padded(const int32_t* input_ids, const uint8_t* loss_mask, const int32_t* cu_seqlens,
+                   int32_t n_traj, int32_t lmax, int32_t pad_id, int32_t* ids_out,
+                   uint8_t* mask_out, int32_t* pos_out, tl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K2 — GRPO group-normalised advantages.
+ * Replaces rl.loss.group_advantages (loss.py:103-116): per group of G >= 2
+ * rewards, mean = fsum(R)/G, var = fsum((R-mean)^2)/G (correctly rounded
+ * sums, as math.fsum), A_i = (R_i - mean) / max(sqrt(var), std_floor).
+ * Groups are contiguous runs of trajectories: group g = [group_off[g],
+ * group_off[g+1]).  Also emits the per-trajectory gradient weight used by
+ * the fused loss (build extension):
+ *   agg = 0 (reference, cli.py:317-344): w_i = 1 / (n_i * G_g * norm_groups)
+ *   agg = 1 (DAPO token-mean):           w_i = 1 / norm_tokens
+ * with n_i = act_off[i+1] - act_off[i] (w_i = 0 when n_i = 0).
+ * adv32 / traj_w / traj_group / act_off may be NULL.
+ * ---------------------------------------------------------------------- */
+int tl_group_advantages(const double* rewards, const int32_t* group_off, int32_t n_groups,
+                        int32_t n_traj, double std_floor, const int32_t* act_off, int32_t agg,
+                        double norm_groups, double norm_tokens, double* adv64, float* adv32,
+                        float* traj_w, int32_t* traj_group, tl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3 — masked clipped surrogate (+ diagnostics, + per-token gradient).
+ * Replaces rl.loss.grpo_multi_turn_loss (loss.py:150-201, use_mask=1),
+ * grpo_single_turn_loss (loss.py:204-227, use_mask=0), unclipped_objective
+ * (loss.py:230-270, objective=1), token_ratio (:119-126), _k3 (:139-147).
+ * ---------------------------------------------------------------------- */
+typedef struct tl_loss_config {
+  double eps_low;      /* LossConfig.epsilon_clip                       */
+  double eps_high;     /* = eps_low in the reference; DAPO clip-higher  */
+  double kl_beta;      /* LossConfig.kl_beta                            */
+  double entropy_coef; /* build extension (LM-head path only)           */
+  int32_t use_mask;    /* 1 multi-turn (A11), 0 single-turn (A13)       */
+  int32_t has_ref;     /* logp_ref present                              */
+  int32_t objective;   /* 0 clipped (A11/A13), 1 unclipped (A14)        */
+  int32_t agg;         /* 0 seq-mean-token-mean (reference), 1 token-mean */
+} tl_loss_config;
+
+/* Per-group result row of the fp64 parity path (TL_GROUP_OUT_LEN doubles):
+ * objective, masked_tokens, total_tokens, clipped, clamp_count, kl_sum,
+ * clip_fraction, kl  (LossDiagnostics, loss.py:67-73). */
+#define TL_GROUP_OUT_LEN 8
+/* Batch report (TL_REPORT_LEN doubles), cli.py:337-345 order first:
+ * 0 objective, 1 clip_fraction, 2 masked_tokens, 3 kl, 4 groups, 5 episodes,
+ * then additive partials for multi-rank reduction:
+ * 6 total_tokens, 7 clamp_count, 8 clipped, 9 kl_sum, 10 entropy_sum,
+ * 11 objective_sum (sum of per-group objectives, or of token terms for
+ *    token-mean aggregation). */
+#define TL_REPORT_LEN 12
+
+/* fp64 parity mode: the reference's operation order (one sequential pass per
+ * group for the sums, IEEE fp64 without contraction, correctly-rounded exp).
+ * Inputs per packed token; grad (nullable) = d objective / d logp_new (A14
+ * for objective=1, the clipped-arm restatement for objective=0). */
+size_t tl_loss_f64_workspace_bytes(int64_t n_tokens);
+int tl_loss_f64(const double* logp_new, const double* logp_old, const double* logp_ref,
+                const uint8_t* mask, const int32_t* cu_seqlens, const int32_t* group_off,
+                const double* adv, int32_t n_traj, int32_t n_groups, int64_t n_tokens,
+                const tl_loss_config* cfg, double* grad, double* group_out, void* workspace,
+                size_t workspace_bytes, tl_stream_t stream);
+/* cli.loss aggregation over per-group rows (cli.py:309-345), reference order. */
+int tl_report_f64(const double* group_out, int32_t n_groups, int32_t n_traj, double* report,
+                  tl_stream_t stream);
+/* Exact-reference elementwise helpers (token_ratio / _k3) for API parity. */
+int tl_token_ratio_f64(const double* logp_new, const double* logp_old, int64_t n, double* ratio,
+                       tl_stream_t stream);
+
+/* fp32 performance mode: per-token terms in fp32, deterministic fixed-order
+ * reductions (per trajectory -> per group -> batch) in fp64.  grad (nullable)
+ * = d objective / d logp_new (report objective, i.e. already scaled by
+ * traj_w).  traj_w from tl_group_advantages. */
+size_t tl_loss_f32_workspace_bytes(int64_t n_tokens, int32_t n_traj, int32_t n_groups);
+int tl_loss_f32(const float* logp_new, const float* logp_old, const float* logp_ref,
+                const uint8_t* mask, const int32_t* traj_of_token, const int32_t* cu_seqlens,
+                const int32_t* group_off, const float* adv32, const float* traj_w,
+                int32_t n_traj, int32_t n_groups, int64_t n_tokens, const tl_loss_config* cfg,
+                float* grad, double* report, void* workspace, size_t workspace_bytes,
+                tl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K4/K5 — fused LM-head log-prob / entropy (+ surrogate epilogue) and its
+ * backward, on tcgen05/TMEM/TMA.  No reference implementation: contract of
+ * PolicyAction.token_logprobs (rollout/policy.py:25-28) / TokenRecord.logp_new
+ * (loss.py:30).  hidden row t predicts target input_ids[t] (caller shifts).
+ * Only action rows (act_idx) are computed; [T, V] logits are never
+ * materialised (vocab is swept in 256-wide tiles with an online
+ * log-sum-exp); tokens are processed in chunks of chunk_rows action rows.
+ * ---------------------------------------------------------------------- */
+size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab, int64_t n_tokens,
+                                 int32_t n_traj, int32_t n_groups);
+/* Forward only: logp/entropy/lse for rows idx[0..n_rows) of hidden
+ * (F3: rollout-side logp_old / logp_ref).  Outputs indexed like idx
+ * (out[k] for row idx[k]); idx NULL = rows 0..n_rows-1. */
+int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int32_t* targets,
+                       const int32_t* idx, int64_t n_rows, int32_t hidden_dim, int32_t vocab,
+                       float* logp, float* entropy, float* lse, int32_t chunk_rows,
+                       void* workspace, size_t workspace_bytes, tl_stream_t stream);
+/* Whole GRPO step on device-resident tensors:
+ *   logp_new = LMhead(hidden[act rows]); surrogate (K3 math) fused into the
+ *   log-prob epilogue; report; loss = -(objective + entropy_coef * mean
+ *   entropy); dhidden = dloss/dhidden (bf16 [T, H], observation rows zeroed),
+ *   dweight = dloss/dW (fp32 [V, H], overwritten).  dhidden/dweight NULL =
+ *   forward + report only. */
+int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const int32_t* input_ids,
+                        const uint8_t* loss_mask, const int32_t* act_idx, int64_t n_act,
+                        const int32_t* traj_of_token, const int32_t* cu_seqlens,
+                        const int32_t* group_off, const float* logp_old, const float* logp_ref,
+                        const float* adv32, const float* traj_w, int64_t n_tokens,
+                        int32_t hidden_dim, int32_t vocab, int32_t n_traj, int32_t n_groups,
+                        const tl_loss_config* cfg, float* logp_out, float* entropy_out,
+                        uint16_t* dhidden, float* dweight, double* report, int32_t chunk_rows,
+                        void* workspace, size_t workspace_bytes, tl_stream_t stream);
+
+/* Plain tcgen05 GEMM (building block, exported for tests):
+ * C[M,N] (+)= A[M,K] * B[N,K]^T with A given K-major ([M,K], lda) or MN-major
+ * ([K,M], lda) and B K-major ([N,K], ldb) or MN-major ([K,N], ldb).
+ * C is bf16 (c_fp32=0) or fp32 (c_fp32=1, accumulate allowed). */
+int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, const uint16_t* B,
+                 int32_t b_mn_major, int64_t ldb, int32_t M, int32_t N, int32_t K, void* C,
+                 int32_t c_fp32, int64_t ldc, int32_t accumulate, tl_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOOLLOOP_B200_H */

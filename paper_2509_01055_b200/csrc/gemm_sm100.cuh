@@ -1,0 +1,349 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a:
+//   D[M, N] = A[M, K] * B[N, K]^T     (bf16 operands, fp32 accumulate in TMEM)
+// with a pluggable epilogue that consumes the fp32 accumulator straight from
+// TMEM.  Both operands may be K-major or MN-major in global memory; TMA
+// (SWIZZLE_128B) stages them into a STAGES-deep shared-memory ring, one
+// elected thread issues tcgen05.mma (M=128, N=BN, K=16), accumulators are
+// double-buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.
+//
+// Warp roles (256 threads):
+//   warp 0      TMA producer (one lane)
+//   warp 1      MMA issuer (one lane)
+//   warp 2      TMEM allocator / deallocator
+//   warp 3      idle
+//   warps 4..7  epilogue: warp (4+q) owns TMEM lanes [32q, 32q+32) = tile rows
+//
+// Work decomposition: a "unit" is (m_tile, a strip of `strip` consecutive
+// n_tiles).  Units are rasterised in groups of `group_m` M-tiles (all strips
+// of the group before the next group) so the ~148 concurrently running units
+// share A and B tiles in L2; unit u runs on CTA u % gridDim.x.  The epilogue
+// sees begin_unit / tile / end_unit so row-wise reductions over a strip (the
+// online log-sum-exp of the LM head) stay in registers.
+#pragma once
+#include "sm100_ptx.cuh"
+
+namespace tl {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kGemmThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+struct GemmShape {
+  int M, N, K;
+  int m_tiles, n_tiles, k_blocks;
+  int strip;      // n-tiles per unit
+  int n_strips;   // ceil(n_tiles / strip)
+  int group_m;    // M-tiles per raster group
+  int n_units;
+};
+
+struct UnitCoord {
+  int m_tile, n_begin, n_count, strip_idx;
+};
+
+__host__ __device__ inline UnitCoord unit_coord(const GemmShape& s, int u) {
+  const int per_full_group = s.group_m * s.n_strips;
+  const int full_groups = s.m_tiles / s.group_m;
+  int mg, rem, rows;
+  if (u < full_groups * per_full_group) {
+    mg = u / per_full_group;
+    rem = u - mg * per_full_group;
+    rows = s.group_m;
+  } else {
+    mg = full_groups;
+    rem = u - full_groups * per_full_group;
+    rows = s.m_tiles - full_groups * s.group_m;
+  }
+  const int strip_idx = rem / rows;
+  const int mi = rem - strip_idx * rows;
+  UnitCoord c;
+  c.m_tile = mg * s.group_m + mi;
+  c.strip_idx = strip_idx;
+  c.n_begin = strip_idx * s.strip;
+  c.n_count = min(s.strip, s.n_tiles - c.n_begin);
+  return c;
+}
+
+inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m) {
+  GemmShape s;
+  s.M = M;
+  s.N = N;
+  s.K = K;
+  s.m_tiles = (M + kBM - 1) / kBM;
+  s.n_tiles = (N + BN - 1) / BN;
+  s.k_blocks = (K + kBK - 1) / kBK;
+  s.strip = strip < 1 ? 1 : (strip > s.n_tiles ? s.n_tiles : strip);
+  s.n_strips = (s.n_tiles + s.strip - 1) / s.strip;
+  s.group_m = group_m < 1 ? 1 : (group_m > s.m_tiles ? s.m_tiles : group_m);
+  s.n_units = s.m_tiles * s.n_strips;
+  return s;
+}
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
+  static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1 KB align
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, const GemmShape shape,
+                      const typename Epi::Params ep) {
+  using Smem = GemmSmem<BN, STAGES>;
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  constexpr uint32_t kIdesc = idesc_bf16(kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Smem::kBarOffset);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4 * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+        const UnitCoord uc = unit_coord(shape, u);
+        const int m0 = uc.m_tile * kBM;
+        for (int t = 0; t < uc.n_count; ++t) {
+          const int n0 = (uc.n_begin + t) * BN;
+          for (int kb = 0; kb < shape.k_blocks; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * Smem::kStageBytes;
+            uint8_t* sb = sa + Smem::kABytes;
+            mbar_arrive_expect_tx(&full_bar[stage], Smem::kStageBytes);
+            const int k0 = kb * kBK;
+            if constexpr (!A_MN) {
+              tma_load_2d(&map_a, &full_bar[stage], sa, k0, m0, pol_a);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_2d(&map_a, &full_bar[stage], sa + j * 8192, m0 + 64 * j, k0, pol_a);
+            }
+            if constexpr (!B_MN) {
+              tma_load_2d(&map_b, &full_bar[stage], sb, k0, n0, pol_b);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(&map_b, &full_bar[stage], sb + j * 8192, n0 + 64 * j, k0, pol_b);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+        const UnitCoord uc = unit_coord(shape, u);
+        for (int t = 0; t < uc.n_count; ++t) {
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < shape.k_blocks; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * Smem::kStageBytes);
+            const uint32_t sb = sa + Smem::kABytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t da = A_MN ? sw128_desc(sa + kk * 2048, 8192, 1024)
+                                       : sw128_desc(sa + kk * 32, 16, 1024);
+              const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
+                                       : sw128_desc(sb + kk * 32, 16, 1024);
+              umma_bf16(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            umma_commit(&empty_bar[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull_bar[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------------------------------------------------- epilogue --
+    const int q = warp - kEpiWarp0;  // TMEM lane quarter
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    typename Epi::State st;
+    for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+      const UnitCoord uc = unit_coord(shape, u);
+      const int row = uc.m_tile * kBM + row_in_tile;
+      Epi::begin_unit(ep, shape, st, row, uc);
+      for (int t = 0; t < uc.n_count; ++t) {
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+        Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
+        tc_fence_before();
+        mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      Epi::end_unit(ep, shape, st, row, uc);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------- epilogue helpers --
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// Plain store of the fp32 accumulator as bf16 (optionally with a row remap),
+// used for the dH GEMM (rows scattered back to packed positions) and tests.
+struct EpiStoreBF16 {
+  struct Params {
+    __nv_bfloat16_raw* out;
+    long long ldo;          // elements
+    const int32_t* row_map; // nullable: out row = row_map[row]
+  };
+  struct State {};
+  __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+  __device__ static void end_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& s, State&, int row, int col0,
+                              uint32_t taddr) {
+    const bool row_ok = row < s.M;
+    long long orow = row;
+    if (row_ok && p.row_map) orow = p.row_map[row];
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      const int cb = col0 + c;
+      __nv_bfloat16_raw* dst = p.out + orow * p.ldo + cb;
+      if (cb + 32 <= s.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[j + 0]), __uint_as_float(r[j + 1]));
+          v.y = pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          v.z = pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+          v.w = pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+          *reinterpret_cast<uint4*>(dst + j) = v;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (cb + j < s.N) {
+            const uint32_t b = pack_bf16x2(__uint_as_float(r[j]), 0.f);
+            dst[j].x = static_cast<unsigned short>(b & 0xFFFFu);
+          }
+        }
+      }
+    }
+  }
+};
+
+// fp32 store or accumulate (out += acc), used for dW across token chunks.
+struct EpiStoreF32 {
+  struct Params {
+    float* out;
+    long long ldo;
+    int accumulate;
+  };
+  struct State {};
+  __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+  __device__ static void end_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& s, State&, int row, int col0,
+                              uint32_t taddr) {
+    const bool row_ok = row < s.M;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      const int cb = col0 + c;
+      float* dst = p.out + static_cast<long long>(row) * p.ldo + cb;
+      if (cb + 32 <= s.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                 __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          if (p.accumulate) {
+            const float4 o = *reinterpret_cast<const float4*>(dst + j);
+            v.x += o.x;
+            v.y += o.y;
+            v.z += o.z;
+            v.w += o.w;
+          }
+          *reinterpret_cast<float4*>(dst + j) = v;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (cb + j < s.N) dst[j] = (p.accumulate ? dst[j] : 0.f) + __uint_as_float(r[j]);
+      }
+    }
+  }
+};
+
+}  // namespace tl

@@ -1,0 +1,602 @@
+// K4/K5 — fused LM-head log-prob / entropy with the GRPO surrogate epilogue,
+// and its backward, on tcgen05 (gemm_sm100.cuh).
+//
+// No reference implementation: the contract is PolicyAction.token_logprobs
+// (rollout/policy.py:25-28) consumed as TokenRecord.logp_new (rl/loss.py:30).
+// Per chunk of C action rows (act_idx[c0 .. c0+C)):
+//   gather      h_c[C, H]  <- hidden[act_idx[c0 + r]]                 (HBM copy)
+//   fwd GEMM    z = h_c W^T tile by tile (128 x 256, K = H) in TMEM; the
+//               epilogue keeps, per row and per vocab strip, the online
+//               log-sum-exp state (max, sum e^(z-max), sum e^(z-max) z) and
+//               the target logit -> partials [n_strips, C]      (z never stored)
+//   combine     merge strips -> lse, logp = z_y - lse, entropy; the GRPO
+//               surrogate (grpo_token.cuh) runs right here on logp_new:
+//               per-token term / k3 / flags and dLoss/dlogp, dLoss/dent
+//   recompute   same GEMM, epilogue writes dS = dLoss/dz (bf16, [C, V])
+//               dS = g (onehot(y) - p) - c p (z - E_p z),  p = e^(z - lse)
+//   dH GEMM     dhidden[act_idx] = dS W          (A K-major, B = W MN-major)
+//   dW GEMM     dW (+)= dS^T h_c                 (A, B MN-major; fp32 RMW)
+// after all chunks: deterministic trajectory -> group -> batch reductions.
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "gemm_sm100.cuh"
+#include "grpo_token.cuh"
+#include "loss_internal.cuh"
+#include "tl_common.cuh"
+
+namespace tl {
+namespace {
+
+constexpr int kBN = 256;
+constexpr int kStages = 4;
+constexpr int kStripsFwd = 9;
+constexpr int kGroupM = 16;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ------------------------------------------------------------------ TMA maps --
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// bf16 matrix stored row-major as [outer, inner] with row stride ld elements;
+// box = {box_inner, box_outer}, SWIZZLE_128B (box_inner * 2 == 128 bytes).
+int make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer, long long ld,
+             int box_inner, int box_outer) {
+  EncodeFn enc = get_encode();
+  TL_REQUIRE(enc, TL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  TL_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, TL_ERR_INVALID_ARG,
+             "TMA base pointer must be 16-byte aligned");
+  TL_REQUIRE((ld * 2) % 16 == 0, TL_ERR_INVALID_ARG, "row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TL_REQUIRE(r == CUDA_SUCCESS, TL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TL_OK;
+}
+
+// Operand map: K-major [rows, K] -> box {64, box_rows}; MN-major [K, MN] -> box {64, 64}.
+int make_operand_map(CUtensorMap* m, const void* ptr, bool mn_major, long long mn, long long k,
+                     long long ld, int box_rows) {
+  if (!mn_major) return make_map(m, ptr, k, mn, ld, 64, box_rows);
+  return make_map(m, ptr, mn, k, ld, 64, 64);
+}
+
+template <bool A_MN, bool B_MN, class Epi>
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
+                const typename Epi::Params& ep, cudaStream_t st) {
+  using Smem = GemmSmem<kBN, kStages>;
+  auto kern = gemm_sm100_kernel<kBN, kStages, A_MN, B_MN, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Smem::kBytes));
+    configured = true;
+  }
+  if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
+  const int grid = s.n_units < num_sms() ? s.n_units : num_sms();
+  kern<<<grid, kGemmThreads, Smem::kBytes, st>>>(ma, mb, s, ep);
+  TL_LAUNCH_CHECK();
+  count_launch();
+  return TL_OK;
+}
+
+// ------------------------------------------------------------- epilogues --
+// Online log-sum-exp over a vocab strip; one thread = one token row.
+struct EpiLseStats {
+  struct Params {
+    const int32_t* targets;  // [C] target id of each chunk row
+    float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
+    int rows;                // C (partials row stride)
+  };
+  struct State {
+    float m, s, t, zy;
+    int y;
+  };
+  __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                    const UnitCoord&) {
+    st.m = -INFINITY;
+    st.s = 0.f;
+    st.t = 0.f;
+    st.zy = -INFINITY;
+    st.y = row < sh.M ? p.targets[row] : -1;
+  }
+  template <int BN>
+  __device__ static void tile(const Params&, const GemmShape& sh, State& st, int, int col0,
+                              uint32_t taddr) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      const int cb = col0 + c;
+      const int nvalid = sh.N - cb;  // columns >= N are padding
+      float cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __uint_as_float(r[j]);
+        if (j < nvalid) cm = fmaxf(cm, v);
+      }
+      const int yl = st.y - cb;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j == yl) st.zy = __uint_as_float(r[j]);
+      if (cm > st.m) {
+        const float f = exp2f((st.m - cm) * kLog2e);
+        st.s *= f;
+        st.t *= f;
+        st.m = cm;
+      }
+      const float mb = st.m * kLog2e;
+      float s = 0.f, t = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __uint_as_float(r[j]);
+        const float e = j < nvalid ? exp2f(fmaf(v, kLog2e, -mb)) : 0.f;
+        s += e;
+        t = fmaf(e, v, t);
+      }
+      st.s += s;
+      st.t += t;
+    }
+  }
+  __device__ static void end_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                  const UnitCoord& uc) {
+    if (row < sh.M)
+      p.part[static_cast<long long>(uc.strip_idx) * p.rows + row] = make_float4(st.m, st.s, st.t, st.zy);
+  }
+};
+
+// dS = dLoss/dz (bf16) from recomputed logits.
+struct EpiDSoftmax {
+  struct Params {
+    const int32_t* targets;
+    const float* lse;
+    const float* g;   // dLoss/dlogp
+    const float* c;   // dLoss/dentropy
+    const float* ez;  // E_p[z]
+    __nv_bfloat16_raw* ds;
+    long long ldd;
+  };
+  struct State {
+    float lse2, g, c, ez;
+    int y;
+  };
+  __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                    const UnitCoord&) {
+    if (row < sh.M) {
+      st.lse2 = p.lse[row] * kLog2e;
+      st.g = p.g[row];
+      st.c = p.c[row];
+      st.ez = p.ez[row];
+      st.y = p.targets[row];
+    } else {
+      st.lse2 = 0.f;
+      st.g = st.c = st.ez = 0.f;
+      st.y = -1;
+    }
+  }
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
+                              uint32_t taddr) {
+    const bool row_ok = row < sh.M;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      const int cb = col0 + c;
+      float d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float z = __uint_as_float(r[j]);
+        const float pr = exp2f(fmaf(z, kLog2e, -st.lse2));
+        float v = -st.g * pr - st.c * pr * (z - st.ez);
+        if (cb + j == st.y) v += st.g;
+        d[j] = v;
+      }
+      __nv_bfloat16_raw* dst = p.ds + static_cast<long long>(row) * p.ldd + cb;
+      if (cb + 32 <= sh.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 v;
+          v.x = pack_bf16x2(d[j + 0], d[j + 1]);
+          v.y = pack_bf16x2(d[j + 2], d[j + 3]);
+          v.z = pack_bf16x2(d[j + 4], d[j + 5]);
+          v.w = pack_bf16x2(d[j + 6], d[j + 7]);
+          *reinterpret_cast<uint4*>(dst + j) = v;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (cb + j < sh.N) dst[j].x = static_cast<unsigned short>(pack_bf16x2(d[j], 0.f) & 0xFFFFu);
+      }
+    }
+  }
+  __device__ static void end_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+};
+
+// ----------------------------------------------------------- small kernels --
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ idx,
+                                   long long n_rows, int row_vec, uint4* __restrict__ dst) {
+  const long long total = n_rows * row_vec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / row_vec;
+    const int c = static_cast<int>(i - r * row_vec);
+    const long long s = idx ? idx[r] : r;
+    dst[i] = __ldg(src + s * row_vec + c);
+  }
+}
+
+__global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                                  long long n, int32_t* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[idx ? idx[i] : i];
+}
+
+struct CombineArgs {
+  const float4* part;
+  int n_strips, rows;
+  const int32_t* idx;  // row -> packed position (nullable: identity)
+  // forward-only outputs (indexed by row)
+  float* logp_row;
+  float* ent_row;
+  float* lse_row;
+  // fused loss (nullable block: forward-only when logp_old == nullptr)
+  const int32_t* traj_of_token;
+  const float* logp_old;
+  const float* logp_ref;
+  const float* adv;
+  const float* traj_w;
+  tl_loss_config cfg;
+  float ent_grad;        // dLoss/dentropy per action token
+  float* logp_out;       // [T]
+  float* ent_out;        // [T]
+  float* term;           // [T]
+  float* k3o;            // [T]
+  uint8_t* flags;        // [T]
+  float* g_row;          // [C]
+  float* c_row;          // [C]
+  float* ez_row;         // [C]
+};
+
+__global__ void combine_kernel(CombineArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.rows) return;
+  float m = -INFINITY, s = 0.f, t = 0.f, zy = -INFINITY;
+  for (int j = 0; j < a.n_strips; ++j) {
+    const float4 q = a.part[static_cast<long long>(j) * a.rows + r];
+    zy = fmaxf(zy, q.w);
+    if (q.x == -INFINITY) continue;
+    if (q.x > m) {
+      const float f = expf(m - q.x);
+      s = s * f + q.y;
+      t = t * f + q.z;
+      m = q.x;
+    } else {
+      const float f = expf(q.x - m);
+      s += q.y * f;
+      t += q.z * f;
+    }
+  }
+  const float lse = m + logf(s);
+  const float ez = t / s;
+  const float logp = zy - lse;
+  const float ent = lse - ez;
+  if (a.logp_row) a.logp_row[r] = logp;
+  if (a.ent_row) a.ent_row[r] = ent;
+  if (a.lse_row) a.lse_row[r] = lse;
+  if (a.logp_old) {
+    const long long p = a.idx ? a.idx[r] : r;
+    const int b = a.traj_of_token[p];
+    const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
+    const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
+    const float rf = a.cfg.has_ref ? a.logp_ref[p] : 0.f;
+    const TokTermF o = grpo_token_f32(logp, a.logp_old[p], rf, a.cfg.has_ref != 0 && rf == rf,
+                                      a.adv[b], lo, hi,
+                                      static_cast<float>(a.cfg.kl_beta), a.cfg.objective);
+    a.logp_out[p] = logp;
+    a.ent_out[p] = ent;
+    a.term[p] = o.term;
+    a.k3o[p] = o.k3;
+    a.flags[p] = o.flags;
+    a.g_row[r] = -o.dterm * a.traj_w[b];  // loss = -objective
+    a.c_row[r] = a.ent_grad;
+    a.ez_row[r] = ez;
+  }
+}
+
+__global__ void zero_obs_rows_kernel(const uint8_t* __restrict__ mask, long long n_tokens,
+                                     int row_vec, uint4* __restrict__ dh) {
+  const long long total = n_tokens * row_vec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long p = i / row_vec;
+    if (!mask[p]) dh[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+__global__ void fill_f32_kernel(float* __restrict__ x, long long n, float v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+int grid_for(long long n, int block) {
+  long long g = (n + block - 1) / block;
+  const long long cap = static_cast<long long>(num_sms()) * 16;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+// --------------------------------------------------------------- workspace --
+struct ChunkWs {
+  uint16_t* h;      // [C, H]
+  float4* part;     // [kStripsFwd, C]
+  int32_t* y;       // [C]
+  float* lse;       // [C]
+  float* g;         // [C]
+  float* c;         // [C]
+  float* ez;        // [C]
+  float* logp;      // [C]
+  float* ent;       // [C]
+  uint16_t* ds;     // [C, Vld]
+  // step-level
+  float* term;      // [T]
+  float* k3o;       // [T]
+  uint8_t* flags;   // [T]
+  double* traj_out; // [B*8]
+  double* group_out;// [G*8]
+};
+
+long long vld_of(int vocab) { return (vocab + 7) / 8 * 8; }
+
+ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool with_bwd) {
+  ChunkWs c{};
+  c.h = w.take<uint16_t>(static_cast<size_t>(C) * H);
+  c.part = w.take<float4>(static_cast<size_t>(kStripsFwd) * C);
+  c.y = w.take<int32_t>(C);
+  c.lse = w.take<float>(C);
+  c.g = w.take<float>(C);
+  c.c = w.take<float>(C);
+  c.ez = w.take<float>(C);
+  c.logp = w.take<float>(C);
+  c.ent = w.take<float>(C);
+  c.ds = with_bwd ? w.take<uint16_t>(static_cast<size_t>(C) * vld_of(V)) : nullptr;
+  c.term = w.take<float>(T);
+  c.k3o = w.take<float>(T);
+  c.flags = w.take<uint8_t>(T);
+  c.traj_out = w.take<double>(static_cast<size_t>(B) * 8);
+  c.group_out = w.take<double>(static_cast<size_t>(G) * TL_GROUP_OUT_LEN);
+  return c;
+}
+
+GemmShape fwd_shape(int rows, int V, int H) {
+  const int n_tiles = (V + kBN - 1) / kBN;
+  const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
+  return make_shape(rows, V, H, kBN, strip, kGroupM);
+}
+
+// z = h_c W^T with the online-LSE epilogue, then merge strips.
+int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int H, int V,
+                         CombineArgs ca, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
+  if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
+  const GemmShape s = fwd_shape(rows, V, H);
+  EpiLseStats::Params ep{c.y, c.part, rows};
+  if (int e = launch_gemm<false, false, EpiLseStats>(ma, mb, s, ep, st)) return e;
+  ca.part = c.part;
+  ca.n_strips = s.n_strips;
+  ca.rows = rows;
+  combine_kernel<<<(rows + 127) / 128, 128, 0, st>>>(ca);
+  TL_LAUNCH_CHECK();
+  count_launch();
+  return TL_OK;
+}
+
+}  // namespace
+}  // namespace tl
+
+using namespace tl;
+
+extern "C" size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
+                                            int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
+  Workspace w{nullptr, 0};
+  carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true);
+  return w.used + 1024;
+}
+
+extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, const uint16_t* B,
+                            int32_t b_mn_major, int64_t ldb, int32_t M, int32_t N, int32_t K,
+                            void* C, int32_t c_fp32, int64_t ldc, int32_t accumulate,
+                            tl_stream_t stream) {
+  TL_REQUIRE(M >= 0 && N >= 0 && K >= 0, TL_ERR_INVALID_ARG, "negative sizes");
+  if (M == 0 || N == 0) return TL_OK;
+  TL_REQUIRE(K > 0, TL_ERR_UNSUPPORTED, "K must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUtensorMap ma, mb;
+  if (int e = make_operand_map(&ma, A, a_mn_major != 0, M, K, lda, kBM)) return e;
+  if (int e = make_operand_map(&mb, B, b_mn_major != 0, N, K, ldb, kBN)) return e;
+  const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM);
+  const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
+  if (c_fp32) {
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
+    switch (sel) {
+      case 0: return launch_gemm<false, false, EpiStoreF32>(ma, mb, s, ep, st);
+      case 1: return launch_gemm<false, true, EpiStoreF32>(ma, mb, s, ep, st);
+      case 2: return launch_gemm<true, false, EpiStoreF32>(ma, mb, s, ep, st);
+      default: return launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st);
+    }
+  }
+  TL_REQUIRE(!accumulate, TL_ERR_UNSUPPORTED, "accumulate needs fp32 C");
+  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr};
+  switch (sel) {
+    case 0: return launch_gemm<false, false, EpiStoreBF16>(ma, mb, s, ep, st);
+    case 1: return launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st);
+    case 2: return launch_gemm<true, false, EpiStoreBF16>(ma, mb, s, ep, st);
+    default: return launch_gemm<true, true, EpiStoreBF16>(ma, mb, s, ep, st);
+  }
+}
+
+extern "C" int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight,
+                                  const int32_t* targets, const int32_t* idx, int64_t n_rows,
+                                  int32_t H, int32_t V, float* logp, float* entropy, float* lse,
+                                  int32_t chunk_rows, void* workspace, size_t workspace_bytes,
+                                  tl_stream_t stream) {
+  TL_REQUIRE(H > 0 && V > 0 && n_rows >= 0 && chunk_rows > 0, TL_ERR_INVALID_ARG, "bad sizes");
+  TL_REQUIRE(H % 8 == 0, TL_ERR_UNSUPPORTED, "hidden must be a multiple of 8");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace w{static_cast<char*>(workspace), workspace_bytes};
+  ChunkWs c = carve(w, chunk_rows, H, V, 0, 0, 0, false);
+  TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "lmhead workspace too small");
+  for (long long c0 = 0; c0 < n_rows; c0 += chunk_rows) {
+    const int rows = static_cast<int>(n_rows - c0 < chunk_rows ? n_rows - c0 : chunk_rows);
+    const int32_t* ci = idx ? idx + c0 : nullptr;
+    gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(hidden) + (idx ? 0 : c0 * H / 8), ci, rows, H / 8,
+        reinterpret_cast<uint4*>(c.h));
+    TL_LAUNCH_CHECK();
+    gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(targets + (idx ? 0 : c0), ci, rows, c.y);
+    TL_LAUNCH_CHECK();
+    count_launch(2);
+    CombineArgs ca{};
+    ca.logp_row = logp + c0;
+    ca.ent_row = entropy ? entropy + c0 : nullptr;
+    ca.lse_row = lse ? lse + c0 : nullptr;
+    if (int e = lmhead_forward_chunk(c, weight, rows, H, V, ca, st)) return e;
+  }
+  return TL_OK;
+}
+
+extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight,
+                                   const int32_t* input_ids, const uint8_t* loss_mask,
+                                   const int32_t* act_idx, int64_t n_act,
+                                   const int32_t* traj_of_token, const int32_t* cu_seqlens,
+                                   const int32_t* group_off, const float* logp_old,
+                                   const float* logp_ref, const float* adv32, const float* traj_w,
+                                   int64_t n_tokens, int32_t H, int32_t V, int32_t n_traj,
+                                   int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
+                                   float* entropy_out, uint16_t* dhidden, float* dweight,
+                                   double* report, int32_t chunk_rows, void* workspace,
+                                   size_t workspace_bytes, tl_stream_t stream) {
+  TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
+  TL_REQUIRE(cfg->use_mask == 1, TL_ERR_UNSUPPORTED, "LM-head step computes action rows only");
+  TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
+  TL_REQUIRE(H > 0 && V > 0 && chunk_rows > 0 && n_act >= 0, TL_ERR_INVALID_ARG, "bad sizes");
+  TL_REQUIRE(H % 64 == 0, TL_ERR_UNSUPPORTED, "hidden must be a multiple of 64");
+  TL_REQUIRE((dhidden == nullptr) == (dweight == nullptr), TL_ERR_INVALID_ARG,
+             "dhidden and dweight are both given or both NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool bwd = dhidden != nullptr;
+  Workspace w{static_cast<char*>(workspace), workspace_bytes};
+  ChunkWs c = carve(w, chunk_rows, H, V, n_tokens, n_traj, n_groups, bwd);
+  TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "lmhead workspace too small (%zu < %zu)", workspace_bytes,
+             w.used);
+  const long long Vld = vld_of(V);
+  const float ent_grad = n_act > 0 ? static_cast<float>(-cfg->entropy_coef / double(n_act)) : 0.f;
+
+  // observation rows: zero their term state and (if training) their dH rows
+  if (n_tokens > 0) {
+    cudaMemsetAsync(c.term, 0, n_tokens * sizeof(float), st);
+    cudaMemsetAsync(c.k3o, 0, n_tokens * sizeof(float), st);
+    cudaMemsetAsync(c.flags, 0, n_tokens, st);
+    // observation positions report logp 0.0 like cli._flat_logps (cli.py:251)
+    cudaMemsetAsync(logp_out, 0, n_tokens * sizeof(float), st);
+    cudaMemsetAsync(entropy_out, 0, n_tokens * sizeof(float), st);
+    if (bwd) {
+      zero_obs_rows_kernel<<<grid_for(n_tokens * H / 8, 256), 256, 0, st>>>(
+          loss_mask, n_tokens, H / 8, reinterpret_cast<uint4*>(dhidden));
+      TL_LAUNCH_CHECK();
+      count_launch();
+    }
+  }
+  if (bwd && n_act == 0) {
+    cudaMemsetAsync(dweight, 0, static_cast<size_t>(V) * H * sizeof(float), st);
+  }
+
+  for (long long c0 = 0; c0 < n_act; c0 += chunk_rows) {
+    const int rows = static_cast<int>(n_act - c0 < chunk_rows ? n_act - c0 : chunk_rows);
+    const int32_t* ci = act_idx + c0;
+    gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(c.h));
+    TL_LAUNCH_CHECK();
+    gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(input_ids, ci, rows, c.y);
+    TL_LAUNCH_CHECK();
+    count_launch(2);
+
+    CombineArgs ca{};
+    ca.idx = ci;
+    ca.traj_of_token = traj_of_token;
+    ca.logp_old = logp_old;
+    ca.logp_ref = logp_ref;
+    ca.adv = adv32;
+    ca.traj_w = traj_w;
+    ca.cfg = *cfg;
+    ca.ent_grad = ent_grad;
+    ca.logp_out = logp_out;
+    ca.ent_out = entropy_out;
+    ca.term = c.term;
+    ca.k3o = c.k3o;
+    ca.flags = c.flags;
+    ca.g_row = c.g;
+    ca.c_row = c.c;
+    ca.ez_row = c.ez;
+    ca.lse_row = c.lse;
+    if (int e = lmhead_forward_chunk(c, weight, rows, H, V, ca, st)) return e;
+    if (!bwd) continue;
+
+    // recompute z -> dS (bf16)
+    {
+      CUtensorMap ma, mb;
+      if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
+      if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
+      const GemmShape s = fwd_shape(rows, V, H);
+      EpiDSoftmax::Params ep{c.y, c.lse, c.g, c.c, c.ez,
+                             reinterpret_cast<__nv_bfloat16_raw*>(c.ds), Vld};
+      if (int e = launch_gemm<false, false, EpiDSoftmax>(ma, mb, s, ep, st)) return e;
+    }
+    // dH rows = dS W  -> scattered to packed positions
+    {
+      CUtensorMap ma, mb;
+      if (int e = make_operand_map(&ma, c.ds, false, rows, V, Vld, kBM)) return e;
+      if (int e = make_operand_map(&mb, weight, true, H, V, H, kBN)) return e;
+      const GemmShape s = make_shape(rows, H, V, kBN, 1, kGroupM);
+      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
+      if (int e = launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st)) return e;
+    }
+    // dW (+)= dS^T h_c
+    {
+      CUtensorMap ma, mb;
+      if (int e = make_operand_map(&ma, c.ds, true, V, rows, Vld, kBM)) return e;
+      if (int e = make_operand_map(&mb, c.h, true, H, rows, H, kBN)) return e;
+      const GemmShape s = make_shape(V, H, rows, kBN, 1, kGroupM);
+      EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
+      if (int e = launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st)) return e;
+    }
+  }
+  return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,
+                           group_off, n_traj, n_groups, cfg->agg, c.traj_out, c.group_out, report,
+                           st);
+}

@@ -1,0 +1,265 @@
+"""Batched GRPO trajectory-to-loss step on device-resident tensors.
+
+    packed  = packing.pack_table(table)                        # K1
+    step    = GRPOStep(hidden_dim, vocab, LossConfig(...))
+    res     = step(packed, group_off, rewards, hidden, weight, logp_old, logp_ref)
+              # K2 advantages -> K4 fused LM-head logp + surrogate -> K5 backward
+
+Reference semantics: cli.loss (cli.py:272-345) drives token_records ->
+group_advantages -> grpo_multi_turn_loss per task_id group and aggregates
+objective = sum_g obj_g / n_groups.  Here one call does the whole batch with
+the log-probs computed by the fused LM head instead of read from a sidecar,
+and returns the trainer-facing loss gradients (loss = -objective).
+Multi-rank: shard whole groups across ranks (parallel.shard_groups), pass the
+global normalisers, and all-reduce the report (parallel.allreduce_report).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .packing import PackedBatch
+from .rl.loss import AGG_TOKEN_MEAN, LossConfig
+
+REPORT_KEYS = ("objective", "clip_fraction", "masked_tokens", "kl", "groups", "episodes",
+               "total_tokens", "clamp_count", "clipped", "kl_sum", "entropy_sum",
+               "objective_sum")
+
+DEFAULT_CHUNK_ROWS = 148 * 128 * 2  # two 128-row M-tiles per SM per vocab strip wave
+
+
+def report_dict(rep) -> dict:
+    vals = rep.tolist() if hasattr(rep, "tolist") else list(rep)
+    d = dict(zip(REPORT_KEYS, vals))
+    for k in ("masked_tokens", "groups", "episodes", "total_tokens", "clamp_count", "clipped"):
+        d[k] = int(d[k])
+    return d
+
+
+class _Workspace:
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device):
+        import torch
+
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = None
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+def _group_sizes(group_off) -> np.ndarray:
+    go = np.asarray(group_off, dtype=np.int64)
+    return np.diff(go)
+
+
+def advantages(rewards, group_off, n_act_per_traj=None, *, std_floor: float = 1e-6,
+               agg: int = 0, norm_groups: float | None = None, norm_tokens: float | None = None,
+               act_off=None, device=None, stream=None):
+    """K2 over a whole batch.  Returns (adv64, adv32, traj_w, traj_group) device
+    tensors.  group_off (host int array) delimits contiguous groups."""
+    import torch
+
+    L = _lib.lib()
+    go = np.asarray(group_off, dtype=np.int32)
+    sizes = _group_sizes(go)
+    if np.any(sizes < 2):
+        from .errors import GroupTooSmall
+
+        g = int(np.argmax(sizes < 2))
+        raise GroupTooSmall(f"group {g}: need at least 2 rewards, got {int(sizes[g])}")
+    device = torch.device(device or "cuda")
+    n_groups = len(go) - 1
+    B = int(go[-1])
+    r = rewards if torch.is_tensor(rewards) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(rewards, dtype=np.float64)))
+    r = r.to(device=device, dtype=torch.float64)
+    d_go = torch.from_numpy(go).to(device)
+    adv64 = torch.empty(B, dtype=torch.float64, device=device)
+    adv32 = torch.empty(B, dtype=torch.float32, device=device)
+    traj_w = torch.empty(B, dtype=torch.float32, device=device)
+    tgroup = torch.empty(B, dtype=torch.int32, device=device)
+    ng = float(norm_groups if norm_groups is not None else n_groups)
+    nt = float(norm_tokens if norm_tokens is not None else 1.0)
+    _lib.check(L.tl_group_advantages(r.data_ptr(), d_go.data_ptr(), n_groups, B, std_floor,
+                                     _lib.ptr(act_off), agg, ng, nt, adv64.data_ptr(),
+                                     adv32.data_ptr(), traj_w.data_ptr(), tgroup.data_ptr(),
+                                     _lib.stream_handle(stream)))
+    return adv64, adv32, traj_w, tgroup, d_go
+
+
+@dataclass
+class StepResult:
+    report: dict
+    report_tensor: "object"   # float64 [TL_REPORT_LEN] on device
+    logp: "object"            # float32 [T] (0 at observation positions)
+    entropy: "object"         # float32 [T]
+    dhidden: "object"         # bf16 [T, H] or None
+    dweight: "object"         # float32 [V, H] or None
+    adv: "object"             # float64 [B]
+
+
+class GRPOStep:
+    """Fused GRPO step: advantages + LM-head log-prob/entropy + surrogate +
+    backward, all on the device.  Reusable across steps (workspace cached)."""
+
+    def __init__(self, hidden_dim: int, vocab: int, cfg: LossConfig | None = None,
+                 chunk_rows: int | None = None):
+        self.H = int(hidden_dim)
+        self.V = int(vocab)
+        self.cfg = cfg or LossConfig()
+        self.chunk_rows = chunk_rows
+        self._ws = _Workspace()
+
+    def workspace_bytes(self, n_act: int, n_tokens: int, n_traj: int, n_groups: int) -> int:
+        L = _lib.lib()
+        return int(L.tl_lmhead_workspace_bytes(self._chunk(n_act), self.H, self.V, n_tokens,
+                                               n_traj, n_groups))
+
+    def _chunk(self, n_act: int) -> int:
+        if self.chunk_rows:
+            return int(self.chunk_rows)
+        return int(min(DEFAULT_CHUNK_ROWS, max(128, (n_act + 127) // 128 * 128)))
+
+    def __call__(self, packed: PackedBatch, group_off, rewards, hidden, weight, logp_old,
+                 logp_ref=None, *, backward: bool = True, norm_groups: float | None = None,
+                 norm_tokens: float | None = None, stream=None, outputs=None,
+                 adv_cache=None, sync_report: bool = True) -> StepResult:
+        import torch
+
+        L = _lib.lib()
+        dev = hidden.device
+        if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+            raise TypeError("hidden and weight must be bfloat16")
+        if hidden.shape != (packed.n_tokens, self.H) or weight.shape != (self.V, self.H):
+            raise ValueError(f"hidden {tuple(hidden.shape)} / weight {tuple(weight.shape)} do not "
+                             f"match T={packed.n_tokens}, H={self.H}, V={self.V}")
+        if logp_old.shape[0] != packed.n_tokens or (logp_ref is not None and
+                                                    logp_ref.shape[0] != packed.n_tokens):
+            from .errors import MaskMismatch
+
+            raise MaskMismatch("logp arrays must have one entry per packed token")
+        cfg = self.cfg
+        agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
+        go = np.asarray(group_off, dtype=np.int32)
+        n_groups = len(go) - 1
+        if adv_cache is None:
+            adv64, adv32, traj_w, _tg, d_go = advantages(
+                rewards, go, std_floor=cfg.std_floor, agg=agg, norm_groups=norm_groups,
+                norm_tokens=norm_tokens if norm_tokens is not None else max(packed.n_act, 1),
+                act_off=packed.act_off, device=dev, stream=stream)
+        else:
+            adv64, adv32, traj_w, d_go = adv_cache
+        T = packed.n_tokens
+        out = outputs or {}
+        logp = out.get("logp")
+        if logp is None:
+            logp = torch.empty(max(T, 1), dtype=torch.float32, device=dev)
+        ent = out.get("entropy")
+        if ent is None:
+            ent = torch.empty(max(T, 1), dtype=torch.float32, device=dev)
+        dh = dw = None
+        if backward:
+            dh = out.get("dhidden")
+            if dh is None:
+                dh = torch.empty((T, self.H), dtype=torch.bfloat16, device=dev)
+            dw = out.get("dweight")
+            if dw is None:
+                dw = torch.empty((self.V, self.H), dtype=torch.float32, device=dev)
+        rep = out.get("report")
+        if rep is None:
+            rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
+        chunk = self._chunk(packed.n_act)
+        ws_bytes = int(L.tl_lmhead_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
+                                                   n_groups))
+        ws = self._ws.get(ws_bytes, dev)
+        c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
+        _lib.check(L.tl_grpo_lmhead_step(
+            hidden.data_ptr(), weight.data_ptr(), packed.input_ids.data_ptr(),
+            packed.loss_mask.data_ptr(), packed.act_idx.data_ptr(), packed.n_act,
+            packed.traj_of_token.data_ptr(), packed.cu_seqlens.data_ptr(), d_go.data_ptr(),
+            logp_old.data_ptr(), _lib.ptr(logp_ref), adv32.data_ptr(), traj_w.data_ptr(), T,
+            self.H, self.V, packed.n_traj, n_groups, c, logp.data_ptr(), ent.data_ptr(),
+            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk, ws.data_ptr(), ws_bytes,
+            _lib.stream_handle(stream)))
+        return StepResult(report=report_dict(rep.cpu()) if sync_report else {}, report_tensor=rep, logp=logp[:T], entropy=ent[:T],
+                          dhidden=dh, dweight=dw, adv=adv64)
+
+
+def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_ref=None,
+              cfg: LossConfig | None = None, *, want_grad: bool = True, stream=None):
+    """Standalone fp32 K3 over a packed batch with given logp_new (e.g. from a
+    sidecar).  Returns (report dict, grad d objective / d logp_new [T])."""
+    import torch
+
+    L = _lib.lib()
+    cfg = cfg or LossConfig()
+    dev = logp_new.device
+    agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
+    go = np.asarray(group_off, dtype=np.int32)
+    n_groups = len(go) - 1
+    _, adv32, traj_w, _, d_go = advantages(rewards, go, std_floor=cfg.std_floor, agg=agg,
+                                           norm_tokens=max(packed.n_act, 1),
+                                           act_off=packed.act_off, device=dev, stream=stream)
+    T = packed.n_tokens
+    grad = torch.empty(max(T, 1), dtype=torch.float32, device=dev) if want_grad else None
+    rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
+    ws_bytes = int(L.tl_loss_f32_workspace_bytes(max(T, 1), packed.n_traj, n_groups))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
+    _lib.check(L.tl_loss_f32(logp_new.data_ptr(), logp_old.data_ptr(), _lib.ptr(logp_ref),
+                             packed.loss_mask.data_ptr(), packed.traj_of_token.data_ptr(),
+                             packed.cu_seqlens.data_ptr(), d_go.data_ptr(), adv32.data_ptr(),
+                             traj_w.data_ptr(), packed.n_traj, n_groups, T, c, _lib.ptr(grad),
+                             rep.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_handle(stream)))
+    return report_dict(rep.cpu()), (grad[:T] if want_grad else None)
+
+
+def lmhead_logprobs(hidden, weight, targets, rows=None, *, chunk_rows: int | None = None,
+                    stream=None):
+    """Forward-only fused LM head (F3: rollout-side logp_old / logp_ref).
+    Returns (logp, entropy, lse) float32 for hidden rows `rows` (default all)."""
+    import torch
+
+    L = _lib.lib()
+    H = hidden.shape[1]
+    V = weight.shape[0]
+    n = hidden.shape[0] if rows is None else rows.shape[0]
+    dev = hidden.device
+    chunk = int(chunk_rows or min(DEFAULT_CHUNK_ROWS, max(128, (n + 127) // 128 * 128)))
+    ws_bytes = int(L.tl_lmhead_workspace_bytes(chunk, H, V, 0, 0, 0))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    logp = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    ent = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    lse = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    _lib.check(L.tl_lmhead_logprobs(hidden.data_ptr(), weight.data_ptr(), targets.data_ptr(),
+                                    _lib.ptr(rows), n, H, V, logp.data_ptr(), ent.data_ptr(),
+                                    lse.data_ptr(), chunk, ws.data_ptr(), ws_bytes,
+                                    _lib.stream_handle(stream)))
+    return logp[:n], ent[:n], lse[:n]
+
+
+def gemm(A, B, *, a_mn_major=False, b_mn_major=False, out=None, out_fp32=False,
+         accumulate=False, stream=None):
+    """tcgen05 GEMM building block: C = A_op @ B_op^T where A_op is A ([M,K])
+    or A^T (A given [K,M] when a_mn_major) and likewise for B ([N,K] / [K,N])."""
+    import torch
+
+    L = _lib.lib()
+    M, K = (A.shape[1], A.shape[0]) if a_mn_major else (A.shape[0], A.shape[1])
+    N = B.shape[1] if b_mn_major else B.shape[0]
+    KB = B.shape[0] if b_mn_major else B.shape[1]
+    if KB != K:
+        raise ValueError("K mismatch")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32 if out_fp32 else torch.bfloat16,
+                          device=A.device)
+    _lib.check(L.tl_gemm_bf16(A.data_ptr(), int(a_mn_major), A.stride(0), B.data_ptr(),
+                              int(b_mn_major), B.stride(0), M, N, K, out.data_ptr(),
+                              int(out.dtype == torch.float32), out.stride(0), int(accumulate),
+                              _lib.stream_handle(stream)))
+    return out

@@ -1,0 +1,411 @@
+"""GPU parity: CUDA kernels (through the C ABI) vs the CPU oracle and the
+reference-generated golden vectors.  Run on a B200 via gpurun (-m gpu).
+
+Tolerances:
+  pack / mask / positions / cu_seqlens / act_idx   bit-exact
+  fp64 advantages   <= 2 ulp (fsum exact; squares are IEEE x*x where CPython's
+                    pow(x, 2) misrounds ~0.09%), >= 95% bitwise
+  fp64 loss         rel 1e-12 (glibc exp misrounds ~0.07%; GPU exp is CR)
+  fp32 loss/adv     rel 1e-5 (north star)
+  LM-head logp      abs 2e-3 vs fp32/fp64 oracle on identical bf16 inputs
+  dH / dW           rel Frobenius 2e-2 (dS rounded to bf16)
+"""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from conftest import decode_records, fx
+from oracle import grpo_oracle as O
+from oracle import pack_oracle as P
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2509_01055_b200 import grpo, packing  # noqa: E402
+from paper_2509_01055_b200.rl import loss as L  # noqa: E402
+from paper_2509_01055_b200.trajectory import Segment, Trajectory  # noqa: E402
+
+
+def _traj(segs):
+    t = Trajectory()
+    for o, toks in segs:
+        t.segments.append(Segment(o, "", list(toks)))
+    return t
+
+
+def _ulps(a, b):
+    if a == b:
+        return 0
+    return abs(a - b) / max(math.ulp(a), math.ulp(b))
+
+
+# ------------------------------------------------------------------ K1 pack --
+
+def test_pack_golden(golden_pack):
+    trajs = [[(o, t) for o, t in c["segments"]] for c in golden_pack]
+    got = packing.pack([_traj(s) for s in trajs])
+    ref = P.pack_varlen(trajs)
+    for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "traj_of_token",
+              "act_off", "act_idx"):
+        assert np.array_equal(getattr(got, k).cpu().numpy(), ref[k]), k
+
+
+def _random_segments(rng, n_traj, max_seg=9, max_len=40, empty_p=0.1):
+    trajs = []
+    for _ in range(n_traj):
+        segs = []
+        n_seg = rng.randint(0, max_seg)
+        for s in range(n_seg):
+            origin = "action" if s % 2 == 0 else "observation"
+            n = 0 if rng.random() < empty_p else rng.randint(1, max_len)
+            segs.append((origin, [rng.randrange(152064) for _ in range(n)]))
+        trajs.append(segs)
+    return trajs
+
+
+def test_pack_random_shuffled_pool():
+    rng = random.Random(11)
+    trajs = _random_segments(rng, 300)
+    table = packing.segment_table([_traj(s) for s in trajs])
+    # scatter the segments through the pool in a random (arrival) order
+    order = list(range(table.n_seg))
+    rng.shuffle(order)
+    pool = np.empty_like(table.token_pool)
+    src = np.empty_like(table.seg_src_off)
+    pos = 0
+    for s in order:
+        n = table.seg_len[s]
+        pool[pos:pos + n] = table.token_pool[table.seg_src_off[s]:table.seg_src_off[s] + n]
+        src[s] = pos
+        pos += n
+    table.token_pool, table.seg_src_off = pool, src
+    got = packing.pack_table(table)
+    ref = P.pack_varlen(trajs)
+    for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "traj_of_token",
+              "act_off", "act_idx"):
+        assert np.array_equal(getattr(got, k).cpu().numpy(), ref[k]), k
+
+
+def test_pack_large_and_padded():
+    rng = np.random.default_rng(5)
+    B = 64
+    trajs = []
+    for b in range(B):
+        segs = []
+        for s in range(int(rng.integers(1, 14))):
+            segs.append(("action" if s % 2 == 0 else "observation",
+                         rng.integers(0, 32000, int(rng.integers(0, 900))).tolist()))
+        trajs.append(segs)
+    got = packing.pack([_traj(s) for s in trajs])
+    ref = P.pack_varlen(trajs)
+    assert np.array_equal(got.input_ids.cpu().numpy(), ref["input_ids"])
+    assert np.array_equal(got.act_idx.cpu().numpy(), ref["act_idx"])
+    ids, mask, pos = packing.pad(got, pad_id=-1)
+    pref = P.pack_padded(trajs, pad_id=-1)
+    assert np.array_equal(ids.cpu().numpy(), pref["input_ids"])
+    assert np.array_equal(mask.cpu().numpy(), pref["loss_mask"])
+    assert np.array_equal(pos.cpu().numpy(), pref["position_ids"])
+
+
+def test_flatten_action_mask_dropin(golden_pack):
+    from paper_2509_01055_b200.trajectory import action_mask, flatten
+
+    for c in golden_pack[:20]:
+        t = _traj([(o, tk) for o, tk in c["segments"]])
+        assert flatten(t) == c["flatten"]
+        assert action_mask(t) == c["action_mask"]
+
+
+def test_pack_empty_batch():
+    got = packing.pack([])
+    assert got.n_tokens == 0 and got.cu_seqlens.cpu().tolist() == [0]
+    got = packing.pack([Trajectory(), _traj([("action", [])])])
+    assert got.cu_seqlens.cpu().tolist() == [0, 0, 0]
+
+
+# ----------------------------------------------------------- K2 advantages --
+
+def test_advantages_golden(golden_adv):
+    bitwise = total = 0
+    for case in golden_adv:
+        r = [fx(x) for x in case["rewards"]]
+        got = L.group_advantages(r, fx(case["std_floor"]))
+        exp = [fx(a) for a in case["adv"]]
+        for a, b in zip(got, exp):
+            total += 1
+            bitwise += a == b
+            assert _ulps(a, b) <= 2 or abs(a - b) < 1e-300, (r, a, b)
+    assert bitwise / total >= 0.95
+
+
+def test_advantages_batched_fp32_and_degenerate():
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(2, 65, 300)
+    go = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    rewards = rng.uniform(-5, 5, go[-1])
+    rewards[go[5]:go[6]] = 0.1      # all-equal, non-dyadic
+    rewards[go[7]:go[8]] = -1.25
+    adv64, adv32, w, tg, _ = grpo.advantages(rewards, go)
+    a64 = adv64.cpu().numpy()
+    a32 = adv32.cpu().numpy()
+    for g in range(len(sizes)):
+        ref = np.asarray(O.group_advantages(rewards[go[g]:go[g + 1]].tolist()))
+        np.testing.assert_allclose(a64[go[g]:go[g + 1]], ref, rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(a32[go[g]:go[g + 1]], ref, rtol=1e-5, atol=1e-6)
+    assert np.all(a64[go[5]:go[6]] == 0.0) and np.all(a64[go[7]:go[8]] == 0.0)
+    assert np.array_equal(tg.cpu().numpy(), np.repeat(np.arange(len(sizes)), sizes))
+
+
+def test_group_too_small_raises():
+    from paper_2509_01055_b200.errors import GroupTooSmall
+
+    with pytest.raises(GroupTooSmall):
+        L.group_advantages([1.0])
+    with pytest.raises(GroupTooSmall):
+        grpo.advantages([1.0, 2.0, 3.0], [0, 2, 3])
+
+
+# ------------------------------------------------------------- K3 fp64 --
+
+def _to_batch(case):
+    trajs = [[L.TokenRecord(*r) for r in decode_records(t)] for t in case["trajectories"]]
+    return L.GroupBatch("g", trajs, [fx(x) for x in case["rewards"]])
+
+
+def _close(a, b, rel=1e-12, abs_=1e-14):
+    return abs(a - b) <= max(rel * max(abs(a), abs(b)), abs_)
+
+
+def test_loss_fp64_golden(golden_losses):
+    n_bitwise = n = 0
+    for case in golden_losses["cases"]:
+        batch = _to_batch(case)
+        cfg = L.LossConfig(epsilon_clip=fx(case["eps"]), kl_beta=fx(case["beta"]))
+        adv = [fx(a) for a in case["adv"]]
+        obj, diag = L.grpo_multi_turn_loss(batch, adv, cfg)
+        n += 1
+        n_bitwise += obj == fx(case["multi"])
+        assert _close(obj, fx(case["multi"])), (obj, fx(case["multi"]))
+        d = case["diag"]
+        assert diag.masked_tokens == d["masked_tokens"]
+        assert diag.total_tokens == d["total_tokens"]
+        assert diag.clamp_count == d["clamp_count"]
+        assert diag.clip_fraction == fx(d["clip_fraction"])
+        assert _close(diag.kl, fx(d["kl"]))
+        assert _close(L.grpo_single_turn_loss(batch, adv, cfg), fx(case["single"]))
+        val, grads = L.unclipped_objective(batch, adv, cfg)
+        assert _close(val, fx(case["unclipped"]))
+        for row, erow in zip(grads, case["unclipped_grads"]):
+            for g, e in zip(row, erow):
+                assert _close(g, fx(e)), (g, fx(e))
+    assert n_bitwise / n >= 0.5  # exp rounding differs from glibc on ~0.07% of calls
+
+
+def test_token_ratio_golden(golden_losses):
+    ok = 0
+    for a, b, r in golden_losses["ratios"]:
+        got = L.token_ratio(L.TokenRecord(0, fx(a), fx(b), 1))
+        assert _ulps(got, fx(r)) <= 1
+        ok += got == fx(r)
+    assert ok >= len(golden_losses["ratios"]) - 2
+
+
+def test_clipped_grad_vs_oracle():
+    rng = random.Random(8)
+    for _ in range(20):
+        trajs = []
+        for _g in range(rng.randint(2, 5)):
+            recs = [(0, rng.uniform(-3, 0), rng.uniform(-3, 0), rng.randrange(2),
+                     rng.uniform(-3, 0)) for _ in range(rng.randint(1, 12))]
+            trajs.append(recs)
+        adv = O.group_advantages([rng.uniform(-1, 1) for _ in trajs])
+        exp = O.clipped_grad(trajs, adv, 0.2, 0.3)
+        batch = L.GroupBatch("g", [[L.TokenRecord(*r) for r in t] for t in trajs], [0.0] * len(trajs))
+        _, got = L.clipped_objective_grad(batch, adv, L.LossConfig(kl_beta=0.3))
+        for gr, er in zip(got, exp):
+            for g, e in zip(gr, er):
+                assert _close(g, e, 1e-12, 1e-15)
+
+
+# ------------------------------------------------------------- K3 fp32 --
+
+def _synthetic_batch(seed, n_groups=24, G=6, with_ref=True):
+    rng = np.random.default_rng(seed)
+    trajs, rewards = [], []
+    for g in range(n_groups):
+        for i in range(G):
+            segs = []
+            for s in range(int(rng.integers(1, 8)) * 2 - 1):
+                n = int(rng.integers(0 if s else 1, 60))
+                segs.append(("action" if s % 2 == 0 else "observation",
+                             rng.integers(0, 1000, n).tolist()))
+            trajs.append(segs)
+        rewards += rng.choice([1.0, -1.0, 0.5, 0.0], G).tolist()
+    T = sum(len(O.flatten(s)) for s in trajs)
+    lold = -rng.exponential(1.0, T)
+    lnew = lold + rng.normal(0, 0.15, T)
+    lref = lold + rng.normal(0, 0.05, T) if with_ref else None
+    go = np.arange(0, n_groups * G + 1, G, dtype=np.int32)
+    return trajs, np.asarray(rewards), go, lnew, lold, lref
+
+
+def _oracle_report(trajs, rewards, go, lnew, lold, lref, eps=0.2, beta=0.0):
+    groups = []
+    pos = 0
+    for g in range(len(go) - 1):
+        recs_g = []
+        for b in range(go[g], go[g + 1]):
+            n = len(O.flatten(trajs[b]))
+            sl = slice(pos, pos + n)
+            recs_g.append(O.token_records(trajs[b], lnew[sl].tolist(), lold[sl].tolist(),
+                                          None if lref is None else lref[sl].tolist()))
+            pos += n
+        groups.append((recs_g, rewards[go[g]:go[g + 1]].tolist()))
+    return O.loss_report(groups, eps, beta), groups
+
+
+def test_loss_fp32_batch_vs_oracle():
+    trajs, rewards, go, lnew, lold, lref = _synthetic_batch(1)
+    packed = packing.pack([_traj(s) for s in trajs])
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    cfg = L.LossConfig(kl_beta=0.1)
+    rep, grad = grpo.grpo_loss(packed, go, rewards, f(lnew), f(lold), f(lref), cfg)
+    ref, groups = _oracle_report(trajs, rewards, go, lnew.astype(np.float32).astype(np.float64),
+                                 lold.astype(np.float32).astype(np.float64),
+                                 lref.astype(np.float32).astype(np.float64), beta=0.1)
+    assert rep["masked_tokens"] == ref["masked_tokens"]
+    assert rep["groups"] == ref["groups"] and rep["episodes"] == ref["episodes"]
+    assert abs(rep["objective"] - ref["objective"]) <= 1e-5 * max(1.0, abs(ref["objective"]))
+    assert abs(rep["kl"] - ref["kl"]) <= 1e-5 * max(1e-3, abs(ref["kl"]))
+    assert abs(rep["clip_fraction"] - ref["clip_fraction"]) <= 2e-3
+    # gradient of the report objective = clipped_grad / n_groups
+    g = grad.cpu().numpy()
+    pos = 0
+    n_groups = len(go) - 1
+    for recs_g, rw in groups:
+        adv = O.group_advantages(rw)
+        eg = O.clipped_grad(recs_g, adv, 0.2, 0.1)
+        for row in eg:
+            for e in row:
+                assert abs(g[pos] - e / n_groups) <= 1e-5 * max(abs(e / n_groups), 1e-4)
+                pos += 1
+
+
+def test_loss_fp32_masking_invariance_bitwise():
+    trajs, rewards, go, lnew, lold, lref = _synthetic_batch(2)
+    packed = packing.pack([_traj(s) for s in trajs])
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    cfg = L.LossConfig(kl_beta=0.1)
+    base, g0 = grpo.grpo_loss(packed, go, rewards, f(lnew), f(lold), f(lref), cfg)
+    m = packed.loss_mask.cpu().numpy() == 0
+    rng = np.random.default_rng(9)
+    for arr in (lnew, lold, lref):
+        arr[m] = rng.uniform(-50, 50, m.sum())
+    pert, g1 = grpo.grpo_loss(packed, go, rewards, f(lnew), f(lold), f(lref), cfg)
+    assert pert == base
+    assert torch.equal(g0, g1)
+
+
+# ---------------------------------------------------------------- GEMM --
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1000, 96, 1024)])
+def test_gemm_vs_torch(a_mn, b_mn, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    Ain = A.t().contiguous() if a_mn else A
+    Bin = B.t().contiguous() if b_mn else B
+    ref = A.float() @ B.float().t()
+    out = grpo.gemm(Ain, Bin, a_mn_major=a_mn, b_mn_major=b_mn, out_fp32=True)
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-3, err
+    out16 = grpo.gemm(Ain, Bin, a_mn_major=a_mn, b_mn_major=b_mn)
+    assert (out16.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+    acc = out.clone()
+    grpo.gemm(Ain, Bin, a_mn_major=a_mn, b_mn_major=b_mn, out=acc, accumulate=True)
+    assert (acc - 2 * ref).abs().max().item() <= 2e-3 * ref.abs().max().item() + 2e-3
+
+
+# ------------------------------------------------------------ K4 / K5 --
+
+def _bf16_np(t):
+    return t.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("T,H,V", [(300, 256, 1000), (129, 128, 4096), (513, 192, 517)])
+def test_lmhead_forward_vs_oracle(T, H, V):
+    from oracle import lmhead_oracle as LH
+
+    g = torch.Generator(device="cuda").manual_seed(T + V)
+    h = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
+    y = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+    logp, ent, lse = grpo.lmhead_logprobs(h, W, y)
+    rl, re, rs = LH.lmhead_forward(_bf16_np(h), _bf16_np(W), y.cpu().numpy())
+    assert np.abs(logp.cpu().numpy() - rl).max() <= 2e-3
+    assert np.abs(ent.cpu().numpy() - re).max() <= 2e-3
+    assert np.abs(lse.cpu().numpy() - rs).max() <= 2e-3
+
+
+def _rel_fro(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256)])
+def test_grpo_lmhead_step_vs_oracle(H, V, chunk):
+    from oracle import lmhead_oracle as LH
+
+    trajs, rewards, go, _, lold, lref = _synthetic_batch(4, n_groups=6, G=4)
+    for tr in trajs:
+        for i, (o, toks) in enumerate(tr):
+            tr[i] = (o, [t % V for t in toks])
+    packed = packing.pack([_traj(s) for s in trajs])
+    T = packed.n_tokens
+    g = torch.Generator(device="cuda").manual_seed(17)
+    h = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    cfg = L.LossConfig(kl_beta=0.1, entropy_coef=0.01)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=chunk)
+    res = step(packed, go, rewards, h, W, f(lold), f(lref))
+    torch.cuda.synchronize()
+    # oracle: logp_new from the LM-head restatement at action rows
+    ids = packed.input_ids.cpu().numpy()
+    act = packed.act_idx.cpu().numpy()
+    hn, Wn = _bf16_np(h), _bf16_np(W)
+    lp, en, _ = LH.lmhead_forward(hn[act], Wn, ids[act])
+    lnew = np.zeros(T)
+    lnew[act] = lp
+    got_lp = res.logp.cpu().numpy()
+    assert np.abs(got_lp[act] - lp).max() <= 2e-3
+    assert np.all(got_lp[packed.loss_mask.cpu().numpy() == 0] == 0.0)
+    lo32 = lold.astype(np.float32).astype(np.float64)
+    lr32 = lref.astype(np.float32).astype(np.float64)
+    ref, groups = _oracle_report(trajs, rewards, go, lnew, lo32, lr32, beta=0.1)
+    rep = res.report
+    assert rep["masked_tokens"] == ref["masked_tokens"]
+    assert abs(rep["objective"] - ref["objective"]) <= 1e-4
+    assert abs(rep["entropy_sum"] - en.sum()) <= 1e-3 * max(1.0, abs(en.sum()))
+    # backward: dLoss/dlogp = -clipped_grad / n_groups ; dLoss/dent = -coef / n_act
+    n_groups = len(go) - 1
+    gl = np.zeros(T)
+    pos = 0
+    for recs_g, rw in groups:
+        for row in O.clipped_grad(recs_g, O.group_advantages(rw), 0.2, 0.1):
+            for e in row:
+                gl[pos] = -e / n_groups
+                pos += 1
+    cg = np.full(len(act), -0.01 / len(act))
+    dH, dW = LH.lmhead_backward(hn[act], Wn, ids[act], gl[act], cg)
+    got_dh = res.dhidden.float().cpu().numpy()
+    assert _rel_fro(got_dh[act], dH) <= 2e-2
+    assert np.all(got_dh[packed.loss_mask.cpu().numpy() == 0] == 0)
+    assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
