@@ -1,0 +1,434 @@
+"""Benchmark: masked GRPO-step tokens/sec (pack + advantage + LM-head log-prob
++ surrogate loss + LM-head backward) on B200, vs the reference's CPU path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = the whole trajectory-to-loss hot path over one synthetic batch of
+BASELINE.json's config (default C2, Qwen2.5-7B shape: 256 prompts x 8
+rollouts, <= 4 tool turns, seq 4k, H 3584, V 152064, bf16):
+  K1 pack (segment table -> varlen batch) -> K2 group advantages ->
+  K4 fused LM-head logp/entropy + GRPO surrogate epilogue -> K5 backward
+  (dS recompute, dH = dS W, dW = dS^T H) -> deterministic reductions
+  [-> N1 report all-reduce, N2 dW all-reduce when N > 1].
+`value` = packed tokens (action + observation) per second over the whole job,
+inputs resident in HBM; `e2e` = the same through the public API with the
+step's host inputs (segment table, logp_old/logp_ref, rewards) copied from
+pinned host memory and the report read back every step (hidden states and
+the LM-head weight are device-resident model tensors).  Multi-GPU: weak
+scaling, each rank owns a C2-sized shard of whole groups (LPT).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "masked GRPO-step tokens/sec (pack+adv+logprob+loss) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "tokens/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops_sustained", 1437.7), d.get("bf16_tflops", 1712.4), \
+            d.get("hbm_gbs", 6452.5), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.f is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.f.flush()
+        rows = [l.split(",") for l in Path(self.f.name).read_text().splitlines() if l.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[2:6]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------- CPU baseline --
+def cpu_baseline(cfg, wl, target_s: float = 12.0, threads: int | None = None):
+    """The reference's CPU path on a bounded sample of the same workload:
+    the oracle port of token_records -> group_advantages ->
+    grpo_multi_turn_loss (pure Python, as toolloop runs it) on one whole group,
+    plus the fp32 numpy LM-head restatement (fwd + bwd, multithreaded BLAS) on
+    a sample of action tokens; tokens/s extrapolated per token."""
+    from oracle import grpo_oracle as O
+    from oracle import lmhead_oracle as LH
+
+    tab = wl.table
+    # --- loss path on group 0
+    b0, b1 = int(wl.group_off[0]), int(wl.group_off[1])
+    segs_all = []
+    pos_pool = tab.token_pool
+    cu = 0
+    starts = []
+    for b in range(b0, b1):
+        segs = []
+        for s in range(tab.traj_seg_off[b], tab.traj_seg_off[b + 1]):
+            o = int(tab.seg_src_off[s])
+            n = int(tab.seg_len[s])
+            segs.append(("action" if tab.seg_is_action[s] else "observation", pos_pool[o:o + n].tolist()))
+        segs_all.append(segs)
+    lens = [sum(len(t) for _, t in s) for s in segs_all]
+    tg = sum(lens)
+    new = (wl.logp_old[:tg] + 0.05).astype(np.float64)  # logp_new stand-in (LM head timed separately)
+    old = wl.logp_old[:tg].astype(np.float64)
+    ref = wl.logp_ref[:tg].astype(np.float64)
+    t0 = time.perf_counter()
+    recs, pos = [], 0
+    for s, n in zip(segs_all, lens):
+        recs.append(O.token_records(s, new[pos:pos + n].tolist(), old[pos:pos + n].tolist(),
+                                    ref[pos:pos + n].tolist()))
+        pos += n
+    adv = O.group_advantages(wl.rewards[b0:b1].tolist())
+    O.multi_turn(recs, adv, 0.2, 0.0)
+    t_loss = time.perf_counter() - t0
+    # --- LM head on a sample of action tokens
+    H, V = cfg.hidden, cfg.vocab
+    rng = np.random.default_rng(7)
+    W = LH.to_bf16_f32((rng.standard_normal((V, H), dtype=np.float32) * 0.02))
+    y = rng.integers(0, V, 4096)
+
+    def run(n):
+        h = LH.to_bf16_f32(rng.standard_normal((n, H), dtype=np.float32))
+        t = time.perf_counter()
+        LH.lmhead_forward(h, W, y[:n], chunk=128)
+        LH.lmhead_backward(h, W, y[:n], np.full(n, -1e-3), None, chunk=128)
+        return time.perf_counter() - t
+
+    # time(n) = fixed (dW alloc/accumulate over V x H) + n * per_token: take the
+    # slope between two sample sizes so the per-step fixed cost (amortised over
+    # a whole batch in a real step) does not inflate the per-token figure.
+    n1 = 64
+    run(n1)  # warm BLAS / page in W
+    t1 = run(n1)
+    n = int(min(4096, max(4 * n1, n1 * target_s / max(t1, 1e-3))))
+    dt = run(n)
+    per_act = max((dt - t1) / (n - n1), dt / n * 0.5)
+    f_act = wl.n_act / max(wl.n_tokens, 1)
+    per_tok = t_loss / tg + f_act * per_act
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas_threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        blas_threads = os.cpu_count() or 1
+    return {
+        "value": 1.0 / per_tok,
+        "unit": UNIT,
+        "cores": int(blas_threads),
+        "kind": "port",
+        "sample": (f"oracle/ port: pure-Python token_records+group_advantages+multi_turn on group 0 "
+                   f"({tg} tokens, {t_loss:.3f}s, 1 core) + numpy fp32 LM-head fwd+bwd on {n} action "
+                   f"tokens at H={H} V={V} ({dt:.2f}s, {blas_threads} BLAS threads); "
+                   f"per-token cost extrapolated with f_act={f_act:.3f}"),
+        "host_cpu": _cpu_model(),
+    }
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except Exception:
+        pass
+    return f"{os.cpu_count()} cpus"
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2509_01055_b200.synthetic import make_workload
+
+    wl = make_workload(cfg, group_ids=np.arange(min(cfg.prompts, 2)))
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, wl, target_s=3.0)
+    vals, last = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        last = cpu_baseline(cfg, wl, target_s=args.ref_seconds)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (loss path) / f32 (LM head)",
+        "data": "synthetic", "config": {"workload": cfg.desc, "name": cfg.name},
+        "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU path --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--chunk-rows", type=int, default=None)
+    args = ap.parse_args()
+
+    from paper_2509_01055_b200.synthetic import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_01055_b200 import _lib, grpo, packing, parallel
+    from paper_2509_01055_b200.rl.loss import AGG_TOKEN_MEAN, LossConfig
+    from paper_2509_01055_b200.synthetic import group_act_tokens, make_workload
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # global batch = world x config (weak scaling); whole groups per rank by LPT
+    n_groups_global = cfg.prompts * world
+    work = group_act_tokens(cfg, np.arange(n_groups_global))
+    shards = parallel.shard_groups(work, world)
+    wl = make_workload(cfg, group_ids=shards[rank])
+    agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
+    loss_cfg = LossConfig(epsilon_clip=0.2, kl_beta=0.04, loss_agg=cfg.loss_agg)
+    norm_tokens = float(work.sum())
+    H, V, T = cfg.hidden, cfg.vocab, wl.n_tokens
+
+    # device-resident inputs
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    hidden = torch.randn((T, H), device=dev, dtype=torch.bfloat16, generator=g)
+    gw = torch.Generator(device=dev).manual_seed(99)  # same W on every rank
+    weight = (torch.randn((V, H), device=dev, dtype=torch.float32, generator=gw) * 0.02).to(torch.bfloat16)
+    tab = wl.table
+    dtab = {k: torch.from_numpy(np.ascontiguousarray(getattr(tab, k))).to(dev)
+            for k in ("token_pool", "seg_src_off", "seg_len", "seg_is_action", "traj_seg_off")}
+    lold = torch.from_numpy(wl.logp_old).to(dev)
+    lref = torch.from_numpy(wl.logp_ref).to(dev)
+    rewards = torch.from_numpy(wl.rewards).to(dev)
+    # Realistic behaviour-policy log-probs: the current policy's logp on the
+    # action rows (forward-only fused LM head) plus a small drift, so ratios,
+    # clip fraction and KL sit where a real GRPO step puts them.
+    packed0 = packing.pack_table(tab, device=dev, validate=True, vocab=V, device_inputs=dtab)
+    lp_now, _, _ = grpo.lmhead_logprobs(hidden, weight, packed0.input_ids, rows=packed0.act_idx)
+    gn = torch.Generator(device=dev).manual_seed(4321 + rank)
+    act_rows = packed0.act_idx.long()
+    lold[act_rows] = lp_now + 0.1 * torch.randn(lp_now.shape, device=dev, generator=gn)
+    lref[act_rows] = lold[act_rows] + 0.05 * torch.randn(lp_now.shape, device=dev, generator=gn)
+    wl.logp_old = lold.cpu().numpy()
+    wl.logp_ref = lref.cpu().numpy()
+    del packed0, lp_now, act_rows
+    step = grpo.GRPOStep(H, V, loss_cfg, chunk_rows=args.chunk_rows)
+    outputs = {
+        "logp": torch.empty(T, dtype=torch.float32, device=dev),
+        "entropy": torch.empty(T, dtype=torch.float32, device=dev),
+        "dhidden": torch.empty((T, H), dtype=torch.bfloat16, device=dev),
+        "dweight": torch.empty((V, H), dtype=torch.float32, device=dev),
+        "report": torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev),
+    }
+
+    def one_step(device_tab, lo, lr, rw):
+        packed = packing.pack_table(tab, device=dev, validate=False, device_inputs=device_tab)
+        res = step(packed, wl.group_off, rw, hidden, weight, lo, lr,
+                   norm_groups=n_groups_global, norm_tokens=norm_tokens, outputs=outputs,
+                   sync_report=False)
+        if world > 1:
+            parallel.allreduce_report(res.report_tensor, agg)
+            parallel.allreduce_grad(res.dweight)
+        return res
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        one_step(dtab, lold, lref, rewards)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region (device-resident inputs; inputs >> L2: hidden is GBs)
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            res = one_step(dtab, lold, lref, rewards)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    rep = grpo.report_dict(res.report_tensor.cpu())
+    tok_global = torch.tensor([T, wl.n_act], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tok_global)
+    T_all, A_all = (float(x) for x in tok_global.tolist())
+    value = T_all / (ms / 1e3)
+
+    # ---- per-kernel device timing (separate, untimed pass)
+    prof = {}
+    if not args.no_profile:
+        _lib.profile_enable(True)
+        one_step(dtab, lold, lref, rewards)
+        torch.cuda.synchronize()
+        prof = _lib.profile_read()
+        _lib.profile_enable(False)
+
+    # ---- end-to-end through the public API with host inputs
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        htab = {k: pin(getattr(tab, k)) for k in dtab}
+        h_lold, h_lref, h_rw = pin(wl.logp_old), pin(wl.logp_ref), pin(wl.rewards)
+        h2d = sum(v.numel() * v.element_size() for v in htab.values()) + \
+            h_lold.numel() * 4 + h_lref.numel() * 4 + h_rw.numel() * 8
+        host_rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            d = {k: v.to(dev, non_blocking=True) for k, v in htab.items()}
+            r = one_step(d, h_lold.to(dev, non_blocking=True), h_lref.to(dev, non_blocking=True),
+                         h_rw.to(dev, non_blocking=True))
+            host_rep.copy_(r.report_tensor, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": T_all / (float(ems.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(host_rep.numel() * 8),
+               "ms_per_step": float(ems.item()),
+               "inputs": "segment table + logp_old/logp_ref + rewards from pinned host memory; "
+                         "hidden states / LM-head weight device-resident (model tensors)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak_s, peak_b, hbm, peak_kind = _peaks()
+    flops_alg = 6.0 * wl.n_act * H * V      # fwd logp (2) + dH (2) + dW (2), action rows only
+    flops_issued = 8.0 * wl.n_act * H * V   # + logits recompute in the backward
+    gemm_ms = sum(prof.get(k, (0, 0))[0] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
+    gemm_launch = sum(prof.get(k, (0, 0))[1] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
+    roofline = None
+    if gemm_ms > 0:
+        ach = flops_alg / (gemm_ms / 1e3) / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": ach, "peak": peak_s, "unit": "TFLOP/s",
+            "frac": ach / peak_s, "traffic": None,
+            "kernel": "gemm_sm100_kernel (tcgen05 LM-head fwd / dS recompute / dH / dW), "
+                      "algorithmic 6*T_act*H*V per step over their summed event time",
+            "launches_per_step": gemm_launch,
+            "issued_frac": flops_issued / (gemm_ms / 1e3) / 1e12 / peak_s,
+            "frac_of_burst_peak": ach / peak_b,
+            "step_frac": (flops_alg / (peak_s * 1e12)) / (ms / 1e3),
+            "peak_kind": f"{peak_kind} bf16 sustained",
+        }
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.desc, "name": cfg.name, "global_batch": cfg.prompts * cfg.n * world,
+                   "seq_len": cfg.seq, "hidden": H, "vocab": V,
+                   "tokens_per_step": int(T_all), "action_tokens_per_step": int(A_all),
+                   "action_tokens_per_s": A_all / (ms / 1e3),
+                   "parallelism": f"dp{world} (groups, LPT)", "l2": "inputs >> L2 (hidden is GBs)",
+                   "chunk_rows": step._chunk(wl.n_act), "loss_agg": cfg.loss_agg},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "kernel_ms_per_step": {k: v[0] for k, v in prof.items() if v[1]},
+        "report": {k: rep[k] for k in ("objective", "clip_fraction", "masked_tokens", "kl")},
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, wl)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,13 @@ const char* tl_last_error(void);
 int tl_abi_version(void);
 /* Number of kernels this library has launched since load (monotonic). */
 int64_t tl_launch_count(void);
+/* Optional device timing per kernel category (CUDA events on the launching
+ * stream).  enable(1) clears and starts recording, enable(0) stops;
+ * read() synchronises the recorded events and returns per-category
+ * milliseconds and launch counts; category(i) names category i. */
+int tl_profile_enable(int32_t on);
+int tl_profile_read(double* ms, int64_t* counts, int32_t n_categories);
+const char* tl_profile_category(int32_t i);
 
 /* ------------------------------------------------------------------------
  * K1 — trajectory packer.
@@ -166,6 +173,15 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
                        const int32_t* idx, int64_t n_rows, int32_t hidden_dim, int32_t vocab,
                        float* logp, float* entropy, float* lse, int32_t chunk_rows,
                        void* workspace, size_t workspace_bytes, tl_stream_t stream);
+/* Backward modes of tl_grpo_lmhead_step.
+ *  STORE_LOGITS: the forward epilogue also writes the chunk's logits as fp16
+ *    into the [chunk_rows, V] workspace; an elementwise pass turns them into
+ *    bf16 dS in place (6*T*H*V issued FLOPs; [T, V] is never allocated — only
+ *    one chunk at a time).
+ *  RECOMPUTE: the backward recomputes the logits with a second GEMM whose
+ *    epilogue writes dS (8*T*H*V issued FLOPs; no logits ever leave TMEM). */
+#define TL_LMHEAD_STORE_LOGITS 0
+#define TL_LMHEAD_RECOMPUTE 1
 /* Whole GRPO step on device-resident tensors:
  *   logp_new = LMhead(hidden[act rows]); surrogate (K3 math) fused into the
  *   log-prob epilogue; report; loss = -(objective + entropy_coef * mean
@@ -180,7 +196,8 @@ int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const in
                         int32_t hidden_dim, int32_t vocab, int32_t n_traj, int32_t n_groups,
                         const tl_loss_config* cfg, float* logp_out, float* entropy_out,
                         uint16_t* dhidden, float* dweight, double* report, int32_t chunk_rows,
-                        void* workspace, size_t workspace_bytes, tl_stream_t stream);
+                        int32_t mode, void* workspace, size_t workspace_bytes,
+                        tl_stream_t stream);
 
 /* Plain tcgen05 GEMM (building block, exported for tests):
  * C[M,N] (+)= A[M,K] * B[N,K]^T with A given K-major ([M,K], lda) or MN-major

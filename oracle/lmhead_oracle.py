@@ -67,7 +67,7 @@ def lmhead_backward(h, W, y, g, c=None, chunk: int = 512):
     T, H = h.shape
     V = W.shape[0]
     dH = np.zeros((T, H), dtype=np.float32)
-    dW = np.zeros((V, H), dtype=np.float64)
+    dW = np.zeros((V, H), dtype=np.float32)
     Wt = np.ascontiguousarray(W.T)
     for s in range(0, T, chunk):
         e = min(T, s + chunk)
@@ -82,5 +82,5 @@ def lmhead_backward(h, W, y, g, c=None, chunk: int = 512):
             dz -= c[s:e, None] * p * (z - ez)
         dz32 = dz.astype(np.float32)
         dH[s:e] = dz32 @ W
-        dW += (dz32.T @ h[s:e]).astype(np.float64)
-    return dH, dW.astype(np.float32)
+        dW += dz32.T @ h[s:e]
+    return dH, dW

@@ -28,6 +28,7 @@ TL_REPORT_LEN = 12
 # Every symbol include/toolloop_b200.h declares (checked by the CPU tests).
 EXPORTS = [
     "tl_last_error", "tl_abi_version", "tl_launch_count",
+    "tl_profile_enable", "tl_profile_read", "tl_profile_category",
     "tl_pack_workspace_bytes", "tl_pack_varlen", "tl_pack_padded",
     "tl_group_advantages",
     "tl_loss_f64_workspace_bytes", "tl_loss_f64", "tl_report_f64", "tl_token_ratio_f64",
@@ -55,6 +56,9 @@ _SIGS = {
     "tl_last_error": (C.c_char_p, []),
     "tl_abi_version": (C.c_int, []),
     "tl_launch_count": (_I64, []),
+    "tl_profile_enable": (C.c_int, [_I32]),
+    "tl_profile_read": (C.c_int, [_P, _P, _I32]),
+    "tl_profile_category": (C.c_char_p, [_I32]),
     "tl_pack_workspace_bytes": (_SZ, [_I32, _I32]),
     "tl_pack_varlen": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _SZ, _P]),
@@ -74,7 +78,7 @@ _SIGS = {
                                      _P]),
     "tl_grpo_lmhead_step": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64,
                                       _I32, _I32, _I32, _I32, C.POINTER(LossConfigC), _P, _P, _P,
-                                      _P, _P, _I32, _P, _SZ, _P]),
+                                      _P, _P, _I32, _I32, _P, _SZ, _P]),
     "tl_gemm_bf16": (C.c_int, [_P, _I32, _I64, _P, _I32, _I64, _I32, _I32, _I32, _P, _I32, _I64,
                                _I32, _P]),
 }
@@ -137,3 +141,23 @@ def stream_handle(stream=None) -> int:
 
 def launch_count() -> int:
     return int(load(False).tl_launch_count())
+
+
+N_PROF = 12
+LMHEAD_STORE_LOGITS = 0
+LMHEAD_RECOMPUTE = 1
+
+
+def profile_enable(on: bool = True) -> None:
+    check(load(False).tl_profile_enable(1 if on else 0))
+
+
+def profile_read() -> dict:
+    """{category: (ms, launches)} for the kernels recorded since enable."""
+    import numpy as np
+
+    L = load(False)
+    ms = np.zeros(N_PROF, dtype=np.float64)
+    cnt = np.zeros(N_PROF, dtype=np.int64)
+    check(L.tl_profile_read(ms.ctypes.data, cnt.ctypes.data, N_PROF))
+    return {L.tl_profile_category(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(N_PROF)}

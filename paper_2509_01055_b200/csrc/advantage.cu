@@ -101,6 +101,7 @@ extern "C" int tl_group_advantages(const double* rewards, const int32_t* group_o
   }
   if (n_groups == 0) return TL_OK;
   const int grid = (n_groups + tl::kAdvWarps - 1) / tl::kAdvWarps;
+  tl::ProfScope prof(tl::PROF_ADV, static_cast<cudaStream_t>(stream));
   tl::group_adv_kernel<<<grid, tl::kAdvWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
       rewards, group_off, n_groups, std_floor, act_off, agg, norm_groups, norm_tokens, adv64,
       adv32, traj_w, traj_group);

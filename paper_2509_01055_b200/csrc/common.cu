@@ -1,6 +1,8 @@
 // Library-wide state: last-error message, launch counter, device query.
 #include <atomic>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "tl_common.cuh"
 
@@ -31,7 +33,81 @@ int num_sms() {
   return cached;
 }
 
+// ---------------------------------------------------------- profiling ----
+namespace {
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_pool;
+const char* kProfNames[PROF_N] = {"pack",     "advantage", "loss",     "reduce",
+                                  "gather",   "gemm_fwd",  "combine",  "gemm_dsoftmax",
+                                  "gemm_dh",  "gemm_dw",   "gemm_other", "dsoftmax"};
+
+cudaEvent_t take_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ev0 = take_event();
+  cudaEventRecord(ev0, st);
+}
+
+ProfScope::~ProfScope() {
+  if (!ev0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t ev1 = take_event();
+  cudaEventRecord(ev1, st);
+  g_prof.push_back({cat, ev0, ev1});
+}
+
 }  // namespace tl
+
+extern "C" int tl_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(tl::g_prof_mu);
+  for (auto& r : tl::g_prof) {
+    tl::g_pool.push_back(r.a);
+    tl::g_pool.push_back(r.b);
+  }
+  tl::g_prof.clear();
+  tl::g_prof_on.store(on != 0);
+  return TL_OK;
+}
+
+extern "C" int tl_profile_read(double* ms, int64_t* counts, int32_t n_cat) {
+  std::lock_guard<std::mutex> lk(tl::g_prof_mu);
+  for (int i = 0; i < n_cat; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  for (auto& r : tl::g_prof) {
+    TL_CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    TL_CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.cat < n_cat) {
+      ms[r.cat] += t;
+      counts[r.cat] += 1;
+    }
+  }
+  return TL_OK;
+}
+
+extern "C" const char* tl_profile_category(int32_t i) {
+  return (i >= 0 && i < tl::PROF_N) ? tl::kProfNames[i] : "";
+}
 
 extern "C" const char* tl_last_error(void) { return tl::g_err; }
 extern "C" int tl_abi_version(void) { return TL_ABI_VERSION; }

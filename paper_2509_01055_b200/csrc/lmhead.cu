@@ -18,6 +18,7 @@
 //   dW GEMM     dW (+)= dS^T h_c                 (A, B MN-major; fp32 RMW)
 // after all chunks: deterministic trajectory -> group -> batch reductions.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <mutex>
 
@@ -84,7 +85,8 @@ int make_operand_map(CUtensorMap* m, const void* ptr, bool mn_major, long long m
 
 template <bool A_MN, bool B_MN, class Epi>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
-                const typename Epi::Params& ep, cudaStream_t st) {
+                const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
+  ProfScope prof(prof_cat, st);
   using Smem = GemmSmem<kBN, kStages>;
   auto kern = gemm_sm100_kernel<kBN, kStages, A_MN, B_MN, Epi>;
   static bool configured = false;
@@ -102,12 +104,38 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
 }
 
 // ------------------------------------------------------------- epilogues --
+__device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// 32 consecutive fp32 accumulator columns -> fp16 (saturating), 4 x 16-byte stores.
+__device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&r)[32], int nvalid) {
+  if (nvalid >= 32) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 v;
+      v.x = pack_f16x2_sat(__uint_as_float(r[j + 0]), __uint_as_float(r[j + 1]));
+      v.y = pack_f16x2_sat(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      v.z = pack_f16x2_sat(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+      v.w = pack_f16x2_sat(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+      *reinterpret_cast<uint4*>(dst + j) = v;
+    }
+  } else {
+    for (int j = 0; j < nvalid; ++j)
+      dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(__uint_as_float(r[j]), 0.f) & 0xFFFFu);
+  }
+}
+
 // Online log-sum-exp over a vocab strip; one thread = one token row.
 struct EpiLseStats {
   struct Params {
     const int32_t* targets;  // [C] target id of each chunk row
     float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
     int rows;                // C (partials row stride)
+    __half_raw* zout;        // optional fp16 logit tile store [C, ldz] (backward input)
+    long long ldz;
   };
   struct State {
     float m, s, t, zy;
@@ -122,7 +150,7 @@ struct EpiLseStats {
     st.y = row < sh.M ? p.targets[row] : -1;
   }
   template <int BN>
-  __device__ static void tile(const Params&, const GemmShape& sh, State& st, int, int col0,
+  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
                               uint32_t taddr) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
@@ -131,6 +159,7 @@ struct EpiLseStats {
       tmem_ld_wait();
       const int cb = col0 + c;
       const int nvalid = sh.N - cb;  // columns >= N are padding
+      if (p.zout && row < sh.M) store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid);
       float cm = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -328,6 +357,38 @@ __global__ void combine_kernel(CombineArgs a) {
   }
 }
 
+// In place: fp16 logits z (written by the forward epilogue) -> bf16
+// dS = g (onehot(y) - p) - c p (z - E_p z), p = exp(z - lse).  One CTA per row.
+__global__ void __launch_bounds__(256)
+    dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec, int V,
+                            const int32_t* __restrict__ y, const float* __restrict__ lse,
+                            const float* __restrict__ g, const float* __restrict__ c,
+                            const float* __restrict__ ez) {
+  const int r = blockIdx.x;
+  const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r], e = ez[r];
+  const int yy = y[r];
+  uint4* row = buf + static_cast<long long>(r) * ld_vec;
+  const int nvec = (V + 7) / 8;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint4 q = row[v];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 h2 = *reinterpret_cast<const __half2*>(&w[k]);
+      const float2 z = __half22float2(h2);
+      const int col = v * 8 + 2 * k;
+      const float p0 = exp2f(fmaf(z.x, kLog2e, -l2)), p1 = exp2f(fmaf(z.y, kLog2e, -l2));
+      float d0 = -gg * p0 - cc * p0 * (z.x - e);
+      float d1 = -gg * p1 - cc * p1 * (z.y - e);
+      if (col == yy) d0 += gg;
+      if (col + 1 == yy) d1 += gg;
+      o[k] = pack_bf16x2(d0, d1);
+    }
+    row[v] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 __global__ void zero_obs_rows_kernel(const uint8_t* __restrict__ mask, long long n_tokens,
                                      int row_vec, uint4* __restrict__ dh) {
   const long long total = n_tokens * row_vec;
@@ -398,18 +459,21 @@ GemmShape fwd_shape(int rows, int V, int H) {
   return make_shape(rows, V, H, kBN, strip, kGroupM);
 }
 
-// z = h_c W^T with the online-LSE epilogue, then merge strips.
+// z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
+// keep the chunk's logits in fp16 for the backward (store mode).
 int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int H, int V,
-                         CombineArgs ca, cudaStream_t st) {
+                         CombineArgs ca, cudaStream_t st, __half_raw* zout = nullptr,
+                         long long ldz = 0) {
   CUtensorMap ma, mb;
   if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
   if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
   const GemmShape s = fwd_shape(rows, V, H);
-  EpiLseStats::Params ep{c.y, c.part, rows};
-  if (int e = launch_gemm<false, false, EpiLseStats>(ma, mb, s, ep, st)) return e;
+  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz};
+  if (int e = launch_gemm<false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD)) return e;
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
+  ProfScope prof(PROF_COMBINE, st);
   combine_kernel<<<(rows + 127) / 128, 128, 0, st>>>(ca);
   TL_LAUNCH_CHECK();
   count_launch();
@@ -499,9 +563,11 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                    int64_t n_tokens, int32_t H, int32_t V, int32_t n_traj,
                                    int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
                                    float* entropy_out, uint16_t* dhidden, float* dweight,
-                                   double* report, int32_t chunk_rows, void* workspace,
-                                   size_t workspace_bytes, tl_stream_t stream) {
+                                   double* report, int32_t chunk_rows, int32_t mode,
+                                   void* workspace, size_t workspace_bytes, tl_stream_t stream) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
+  TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE, TL_ERR_INVALID_ARG,
+             "unknown lmhead mode %d", mode);
   TL_REQUIRE(cfg->use_mask == 1, TL_ERR_UNSUPPORTED, "LM-head step computes action rows only");
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(H > 0 && V > 0 && chunk_rows > 0 && n_act >= 0, TL_ERR_INVALID_ARG, "bad sizes");
@@ -539,12 +605,15 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   for (long long c0 = 0; c0 < n_act; c0 += chunk_rows) {
     const int rows = static_cast<int>(n_act - c0 < chunk_rows ? n_act - c0 : chunk_rows);
     const int32_t* ci = act_idx + c0;
-    gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
-        reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(c.h));
-    TL_LAUNCH_CHECK();
-    gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(input_ids, ci, rows, c.y);
-    TL_LAUNCH_CHECK();
-    count_launch(2);
+    {
+      ProfScope prof(PROF_GATHER, st);
+      gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
+          reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(c.h));
+      TL_LAUNCH_CHECK();
+      gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(input_ids, ci, rows, c.y);
+      TL_LAUNCH_CHECK();
+      count_launch(2);
+    }
 
     CombineArgs ca{};
     ca.idx = ci;
@@ -564,18 +633,28 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     ca.c_row = c.c;
     ca.ez_row = c.ez;
     ca.lse_row = c.lse;
-    if (int e = lmhead_forward_chunk(c, weight, rows, H, V, ca, st)) return e;
+    const bool store = bwd && mode == TL_LMHEAD_STORE_LOGITS;
+    if (int e = lmhead_forward_chunk(c, weight, rows, H, V, ca, st,
+                                     store ? reinterpret_cast<__half_raw*>(c.ds) : nullptr, Vld))
+      return e;
     if (!bwd) continue;
 
-    // recompute z -> dS (bf16)
-    {
+    if (store) {
+      // fp16 chunk logits -> bf16 dS in place (elementwise, HBM-bound)
+      ProfScope prof(PROF_DSOFTMAX, st);
+      dsoftmax_inplace_kernel<<<rows, 256, 0, st>>>(reinterpret_cast<uint4*>(c.ds), Vld / 8, V, c.y,
+                                                    c.lse, c.g, c.c, c.ez);
+      TL_LAUNCH_CHECK();
+      count_launch();
+    } else {
+      // recompute z -> dS (bf16) in the GEMM epilogue
       CUtensorMap ma, mb;
       if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
       if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
       const GemmShape s = fwd_shape(rows, V, H);
       EpiDSoftmax::Params ep{c.y, c.lse, c.g, c.c, c.ez,
                              reinterpret_cast<__nv_bfloat16_raw*>(c.ds), Vld};
-      if (int e = launch_gemm<false, false, EpiDSoftmax>(ma, mb, s, ep, st)) return e;
+      if (int e = launch_gemm<false, false, EpiDSoftmax>(ma, mb, s, ep, st, PROF_GEMM_DS)) return e;
     }
     // dH rows = dS W  -> scattered to packed positions
     {
@@ -584,7 +663,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       if (int e = make_operand_map(&mb, weight, true, H, V, H, kBN)) return e;
       const GemmShape s = make_shape(rows, H, V, kBN, 1, kGroupM);
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
-      if (int e = launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st)) return e;
+      if (int e = launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st, PROF_GEMM_DH)) return e;
     }
     // dW (+)= dS^T h_c
     {
@@ -593,7 +672,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       if (int e = make_operand_map(&mb, c.h, true, H, rows, H, kBN)) return e;
       const GemmShape s = make_shape(V, H, rows, kBN, 1, kGroupM);
       EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
-      if (int e = launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st)) return e;
+      if (int e = launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st, PROF_GEMM_DW)) return e;
     }
   }
   return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,

@@ -338,6 +338,7 @@ int launch_reductions(const float* term, const float* k3o, const uint8_t* flags,
                       const uint8_t* mask, int use_mask, const int32_t* cu, const int32_t* group_off,
                       int n_traj, int n_groups, int agg, double* traj_out, double* group_out,
                       double* report, cudaStream_t st) {
+  ProfScope prof(PROF_REDUCE, st);
   if (n_traj > 0) {
     traj_reduce_kernel<<<n_traj, 256, 0, st>>>(term, k3o, flags, ent, mask, use_mask, cu, traj_out);
     TL_LAUNCH_CHECK();
@@ -393,6 +394,7 @@ extern "C" int tl_loss_f64(const double* logp_new, const double* logp_old, const
   uint8_t* flags = w.take<uint8_t>(n_tokens);
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "loss_f64 workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  tl::ProfScope prof(tl::PROF_LOSS, st);
   if (n_traj > 0) {
     tl::loss64_token_kernel<<<n_traj, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, cu_seqlens,
                                                     adv, *cfg, term, k3o, dterm, flags);
@@ -458,6 +460,7 @@ extern "C" int tl_loss_f32(const float* logp_new, const float* logp_old, const f
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "loss_f32 workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n_tokens > 0) {
+    tl::ProfScope prof(tl::PROF_LOSS, st);
     const long long blocks = (n_tokens + 255) / 256;
     const int grid = static_cast<int>(blocks > 148 * 16 ? 148 * 16 : blocks);
     tl::loss32_token_kernel<<<grid, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, traj_of_token,

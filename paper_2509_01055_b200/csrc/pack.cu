@@ -202,6 +202,7 @@ extern "C" int tl_pack_varlen(const int32_t* token_pool, const int32_t* seg_src_
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "pack workspace too small (%zu < %zu)", workspace_bytes,
              w.used);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  tl::ProfScope prof(tl::PROF_PACK, st);
   tl::pack_scan_kernel<<<1, tl::kScanThreads, 0, st>>>(seg_len, seg_is_action, traj_seg_off, n_traj,
                                                        n_seg, seg_dst, seg_act, seg_traj, cu_seqlens,
                                                        act_off);

@@ -64,4 +64,30 @@ int num_sms();
 // bench.py can report `gpu_launches` from the library itself.
 void count_launch(int n = 1);
 
+// Optional per-category device timing (tl_profile_enable): a ProfScope
+// records a CUDA event pair on the launching stream around the kernels it
+// encloses; tl_profile_read() resolves and sums them.  Disabled = no-op.
+enum ProfCat {
+  PROF_PACK = 0,
+  PROF_ADV,
+  PROF_LOSS,
+  PROF_REDUCE,
+  PROF_GATHER,
+  PROF_GEMM_FWD,
+  PROF_COMBINE,
+  PROF_GEMM_DS,
+  PROF_GEMM_DH,
+  PROF_GEMM_DW,
+  PROF_GEMM_OTHER,
+  PROF_DSOFTMAX,
+  PROF_N
+};
+struct ProfScope {
+  int cat;
+  cudaStream_t st;
+  cudaEvent_t ev0 = nullptr;
+  ProfScope(int c, cudaStream_t s);
+  ~ProfScope();
+};
+
 }  // namespace tl

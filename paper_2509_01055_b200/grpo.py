@@ -108,11 +108,15 @@ class GRPOStep:
     backward, all on the device.  Reusable across steps (workspace cached)."""
 
     def __init__(self, hidden_dim: int, vocab: int, cfg: LossConfig | None = None,
-                 chunk_rows: int | None = None):
+                 chunk_rows: int | None = None, recompute: bool = False):
+        """recompute=False keeps each chunk's logits in fp16 for the backward
+        (6*T*H*V FLOPs); True recomputes them in a second GEMM (8*T*H*V) so no
+        logit ever leaves TMEM (include/toolloop_b200.h, TL_LMHEAD_*)."""
         self.H = int(hidden_dim)
         self.V = int(vocab)
         self.cfg = cfg or LossConfig()
         self.chunk_rows = chunk_rows
+        self.mode = _lib.LMHEAD_RECOMPUTE if recompute else _lib.LMHEAD_STORE_LOGITS
         self._ws = _Workspace()
 
     def workspace_bytes(self, n_act: int, n_tokens: int, n_traj: int, n_groups: int) -> int:
@@ -184,7 +188,7 @@ class GRPOStep:
             packed.traj_of_token.data_ptr(), packed.cu_seqlens.data_ptr(), d_go.data_ptr(),
             logp_old.data_ptr(), _lib.ptr(logp_ref), adv32.data_ptr(), traj_w.data_ptr(), T,
             self.H, self.V, packed.n_traj, n_groups, c, logp.data_ptr(), ent.data_ptr(),
-            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk, ws.data_ptr(), ws_bytes,
+            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk, self.mode, ws.data_ptr(), ws_bytes,
             _lib.stream_handle(stream)))
         return StepResult(report=report_dict(rep.cpu()) if sync_report else {}, report_tensor=rep, logp=logp[:T], entropy=ent[:T],
                           dhidden=dh, dweight=dw, adv=adv64)

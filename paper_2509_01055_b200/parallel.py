@@ -1,0 +1,77 @@
+"""Data parallelism by trajectory group (one process per GPU).
+
+Groups are independent units: advantages need only the group's rewards
+(rl/loss.py:103-116) and the batch objective is a sum over groups
+(cli.py:317-344), which SPEC.md:496 states is safe to evaluate in parallel.
+So whole groups are assigned to ranks (LPT: longest-processing-time-first on
+the group's action-token count, the LM head's work), every rank runs the
+fused step on its shard with the GLOBAL normalisers (n_groups, action
+tokens), and the only collectives are
+  N1  all-reduce of the report's additive partials (~12 doubles), and
+  N2  all-reduce of dW (the LM-head weight gradient) when it is trained.
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+# indices into the TL_REPORT_LEN report (include/toolloop_b200.h)
+_ADDITIVE = (2, 4, 5, 6, 7, 8, 9, 10, 11)
+
+
+def shard_groups(work: np.ndarray, world: int) -> list[np.ndarray]:
+    """LPT assignment of groups (by `work`) to `world` ranks.  Deterministic:
+    ties broken by group index; each rank's groups are returned sorted."""
+    work = np.asarray(work)
+    order = sorted(range(len(work)), key=lambda g: (-work[g], g))
+    heap = [(0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for g in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(g)
+        heapq.heappush(heap, (load + int(work[g]), r))
+    return [np.asarray(sorted(o), dtype=np.int64) for o in out]
+
+
+def finalize_report(rep: np.ndarray, agg: int = 0) -> np.ndarray:
+    """Recompute the ratio fields (0 objective, 1 clip_fraction, 3 kl) from
+    the additive partials after a cross-rank sum."""
+    rep = np.array(rep, dtype=np.float64, copy=True)
+    masked, groups = rep[2], rep[4]
+    if agg == 1:
+        rep[0] = rep[11] / masked if masked > 0 else 0.0
+    else:
+        rep[0] = rep[11] / groups if groups > 0 else 0.0
+    rep[1] = rep[8] / masked if masked > 0 else 0.0
+    rep[3] = rep[9] / masked if masked > 0 else 0.0
+    return rep
+
+
+def allreduce_report(rep_tensor, agg: int = 0, group=None):
+    """N1: sum the additive report fields over ranks (in place) and recompute
+    the ratios.  Works for NCCL (device tensor) and gloo (CPU tensor)."""
+    import torch
+    import torch.distributed as dist
+
+    idx = torch.tensor(_ADDITIVE, device=rep_tensor.device)
+    part = rep_tensor.index_select(0, idx)
+    dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    rep_tensor.index_copy_(0, idx, part)
+    masked, groups = rep_tensor[2], rep_tensor[4]
+    if agg == 1:
+        rep_tensor[0] = torch.where(masked > 0, rep_tensor[11] / masked.clamp_min(1), 0.0)
+    else:
+        rep_tensor[0] = torch.where(groups > 0, rep_tensor[11] / groups.clamp_min(1), 0.0)
+    rep_tensor[1] = torch.where(masked > 0, rep_tensor[8] / masked.clamp_min(1), 0.0)
+    rep_tensor[3] = torch.where(masked > 0, rep_tensor[9] / masked.clamp_min(1), 0.0)
+    return rep_tensor
+
+
+def allreduce_grad(t, group=None):
+    """N2: sum a gradient tensor over ranks (the LM-head dW)."""
+    import torch.distributed as dist
+
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t

@@ -315,7 +315,7 @@ def test_loss_fp32_masking_invariance_bitwise():
 # ---------------------------------------------------------------- GEMM --
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1000, 96, 1024)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (304, 520, 200), (1000, 96, 1024), (136, 64, 3584)])
 def test_gemm_vs_torch(a_mn, b_mn, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
@@ -359,8 +359,9 @@ def _rel_fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256)])
-def test_grpo_lmhead_step_vs_oracle(H, V, chunk):
+@pytest.mark.parametrize("recompute", [False, True])
+@pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256), (192, 517, 128)])
+def test_grpo_lmhead_step_vs_oracle(H, V, chunk, recompute):
     from oracle import lmhead_oracle as LH
 
     trajs, rewards, go, _, lold, lref = _synthetic_batch(4, n_groups=6, G=4)
@@ -374,7 +375,7 @@ def test_grpo_lmhead_step_vs_oracle(H, V, chunk):
     W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
     f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
     cfg = L.LossConfig(kl_beta=0.1, entropy_coef=0.01)
-    step = grpo.GRPOStep(H, V, cfg, chunk_rows=chunk)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=chunk, recompute=recompute)
     res = step(packed, go, rewards, h, W, f(lold), f(lref))
     torch.cuda.synchronize()
     # oracle: logp_new from the LM-head restatement at action rows
