@@ -3,29 +3,40 @@
 // with a pluggable epilogue that consumes the fp32 accumulator straight from
 // TMEM.  Both operands may be K-major or MN-major in global memory; TMA
 // (SWIZZLE_128B) stages them into a STAGES-deep shared-memory ring, one
-// elected thread issues tcgen05.mma (M=128, N=BN, K=16), accumulators are
-// double-buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps
-// the MMAs of tile i+1.
+// elected thread issues tcgen05.mma (K=16), accumulators are double-buffered
+// in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of
+// tile i+1.
 //
-// Warp roles (256 threads):
-//   warp 0      TMA producer (one lane)
-//   warp 1      MMA issuer (one lane)
+// CG = 1: one CTA per tile, UMMA 128 x BN.
+// CG = 2: a 2-CTA cluster (one TPC) per tile, UMMA 256 x BN issued by the
+//   leader (tcgen05.mma.cta_group::2): each CTA stages its own 128 A rows and
+//   HALF of the B tile, so per-SM shared-memory fill and L2 reads per FLOP
+//   drop by a third versus CG = 1 (the step is power-capped, so bytes moved per
+//   FLOP set the clock).  TMA completion is counted on the leader's barrier,
+//   MMA completion is multicast to both CTAs' barriers, the peer's epilogue
+//   signals the leader's TMEM-empty barrier remotely.
+//
+// Warp roles (256 threads per CTA):
+//   warp 0      TMA producer (one lane)            [both CTAs]
+//   warp 1      MMA issuer (one lane)              [leader only]
 //   warp 2      TMEM allocator / deallocator
 //   warp 3      idle
 //   warps 4..7  epilogue: warp (4+q) owns TMEM lanes [32q, 32q+32) = tile rows
 //
-// Work decomposition: a "unit" is (m_tile, a strip of `strip` consecutive
-// n_tiles).  Units are rasterised in groups of `group_m` M-tiles (all strips
-// of the group before the next group) so the ~148 concurrently running units
-// share A and B tiles in L2; unit u runs on CTA u % gridDim.x.  The epilogue
-// sees begin_unit / tile / end_unit so row-wise reductions over a strip (the
-// online log-sum-exp of the LM head) stay in registers.
+// Work decomposition: a "unit" is (m_tile of 128*CG rows, a strip of `strip`
+// consecutive n_tiles).  Units are rasterised in groups of `group_m` M-tiles
+// (all strips of the group before the next group) so the concurrently running
+// units share A and B tiles in L2; unit u runs on CTA(-pair) u % n_pairs.  The
+// epilogue sees begin_unit / tile / end_unit so row-wise reductions over a
+// strip (the online log-sum-exp of the LM head) stay in registers.
 #pragma once
+#include <cuda_bf16.h>
+
 #include "sm100_ptx.cuh"
 
 namespace tl {
 
-constexpr int kBM = 128;
+constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;
 constexpr int kGemmThreads = 256;
 constexpr int kEpiWarp0 = 4;
@@ -37,6 +48,7 @@ struct GemmShape {
   int n_strips;   // ceil(n_tiles / strip)
   int group_m;    // M-tiles per raster group
   int n_units;
+  int cg;         // CTAs per tile (M rows per tile = 128 * cg)
 };
 
 struct UnitCoord {
@@ -66,12 +78,13 @@ __host__ __device__ inline UnitCoord unit_coord(const GemmShape& s, int u) {
   return c;
 }
 
-inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m) {
+inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m, int cg = 1) {
   GemmShape s;
   s.M = M;
   s.N = N;
   s.K = K;
-  s.m_tiles = (M + kBM - 1) / kBM;
+  s.cg = cg;
+  s.m_tiles = (M + kBM * cg - 1) / (kBM * cg);
   s.n_tiles = (N + BN - 1) / BN;
   s.k_blocks = (K + kBK - 1) / kBK;
   s.strip = strip < 1 ? 1 : (strip > s.n_tiles ? s.n_tiles : strip);
@@ -81,25 +94,28 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m)
   return s;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBRows = BN / CG;  // B rows staged by each CTA
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
   static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1 KB align
 };
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, class Epi>
+template <int BN, int STAGES, int CG, bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const GemmShape shape,
                       const typename Epi::Params ep) {
-  using Smem = GemmSmem<BN, STAGES>;
+  using Smem = GemmSmem<BN, STAGES, CG>;
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(CG == 1 || CG == 2, "CG");
+  static_assert(Smem::kBRows % 64 == 0, "B half tile must be a multiple of 64 rows");
   constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  constexpr uint32_t kIdesc = idesc_bf16(kBM, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+  constexpr uint32_t kIdesc = idesc_bf16(kBM * CG, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -112,6 +128,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int pair = CG == 2 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int n_pairs = CG == 2 ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -122,47 +141,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4 * 32);
+      mbar_init(&tempty_bar[b], 4 * CG);  // one arrive per epilogue warp of the pair
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_cg2<kTmemCols>(tmem_slot);
+    else tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     if (lane == 0) {
-      const uint64_t pol_a = policy_evict_last();
-      const uint64_t pol_b = policy_evict_last();
+      const uint64_t pol = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+      for (int u = pair; u < shape.n_units; u += n_pairs) {
         const UnitCoord uc = unit_coord(shape, u);
-        const int m0 = uc.m_tile * kBM;
+        const int m0 = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM;
         for (int t = 0; t < uc.n_count; ++t) {
-          const int n0 = (uc.n_begin + t) * BN;
+          const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
           for (int kb = 0; kb < shape.k_blocks; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * Smem::kStageBytes;
             uint8_t* sb = sa + Smem::kABytes;
-            mbar_arrive_expect_tx(&full_bar[stage], Smem::kStageBytes);
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * Smem::kStageBytes);
             const int k0 = kb * kBK;
+            auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1) {
+              if constexpr (CG == 2) tma_load_2d_cg2(m, &full_bar[stage], dst, c0, c1, pol);
+              else tma_load_2d(m, &full_bar[stage], dst, c0, c1, pol);
+            };
             if constexpr (!A_MN) {
-              tma_load_2d(&map_a, &full_bar[stage], sa, k0, m0, pol_a);
+              load(&map_a, sa, k0, m0);
             } else {
 #pragma unroll
-              for (int j = 0; j < kBM / 64; ++j)
-                tma_load_2d(&map_a, &full_bar[stage], sa + j * 8192, m0 + 64 * j, k0, pol_a);
+              for (int j = 0; j < kBM / 64; ++j) load(&map_a, sa + j * 8192, m0 + 64 * j, k0);
             }
             if constexpr (!B_MN) {
-              tma_load_2d(&map_b, &full_bar[stage], sb, k0, n0, pol_b);
+              load(&map_b, sb, k0, n0);
             } else {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(&map_b, &full_bar[stage], sb + j * 8192, n0 + 64 * j, k0, pol_b);
+              for (int j = 0; j < Smem::kBRows / 64; ++j) load(&map_b, sb + j * 8192, n0 + 64 * j, k0);
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -174,12 +198,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+      for (int u = pair; u < shape.n_units; u += n_pairs) {
         const UnitCoord uc = unit_coord(shape, u);
         for (int t = 0; t < uc.n_count; ++t) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -196,15 +220,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                        : sw128_desc(sa + kk * 32, 16, 1024);
               const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
                                        : sw128_desc(sb + kk * 32, 16, 1024);
-              umma_bf16(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+              if constexpr (CG == 2) umma_bf16_cg2(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+              else umma_bf16(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
             }
-            umma_commit(&empty_bar[stage]);
+            if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage]);
+            else umma_commit(&empty_bar[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit(&tfull_bar[acc]);
+          if constexpr (CG == 2) umma_commit_cg2_mc(&tfull_bar[acc]);
+          else umma_commit(&tfull_bar[acc]);
           if (++acc == 2) {
             acc = 0;
             acc_phase ^= 1;
@@ -219,9 +246,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     typename Epi::State st;
-    for (int u = blockIdx.x; u < shape.n_units; u += gridDim.x) {
+    for (int u = pair; u < shape.n_units; u += n_pairs) {
       const UnitCoord uc = unit_coord(shape, u);
-      const int row = uc.m_tile * kBM + row_in_tile;
+      const int row = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM + row_in_tile;
       Epi::begin_unit(ep, shape, st, row, uc);
       for (int t = 0; t < uc.n_count; ++t) {
         mbar_wait(&tfull_bar[acc], acc_phase);
@@ -229,7 +256,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
         Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
         tc_fence_before();
-        mbar_arrive(&tempty_bar[acc]);
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -240,10 +271,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_cg2<kTmemCols>(tmem_base);
+    else tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 

@@ -31,7 +31,8 @@ namespace tl {
 namespace {
 
 constexpr int kBN = 256;
-constexpr int kStages = 4;
+constexpr int kCG = 2;  // 2-CTA (cta_group::2) tiles of 256 x 256
+constexpr int kStages = 6;
 constexpr int kStripsFwd = 9;
 constexpr int kGroupM = 16;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -83,22 +84,46 @@ int make_operand_map(CUtensorMap* m, const void* ptr, bool mn_major, long long m
   return make_map(m, ptr, mn, k, ld, 64, 64);
 }
 
-template <bool A_MN, bool B_MN, class Epi>
+// Operand maps for a GEMM run with CTA group `cg`: A tiles are 128 rows per
+// CTA, B tiles BN/cg rows per CTA (K-major); MN-major boxes are 64 x 64.
+int make_ab_maps(CUtensorMap* ma, CUtensorMap* mb, const void* A, bool a_mn, long long M,
+                 long long lda, const void* B, bool b_mn, long long N, long long ldb, long long K,
+                 int cg) {
+  if (int e = make_operand_map(ma, A, a_mn, M, K, lda, kBM)) return e;
+  return make_operand_map(mb, B, b_mn, N, K, ldb, kBN / cg);
+}
+
+template <int CG, bool A_MN, bool B_MN, class Epi>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
                 const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
   ProfScope prof(prof_cat, st);
-  using Smem = GemmSmem<kBN, kStages>;
-  auto kern = gemm_sm100_kernel<kBN, kStages, A_MN, B_MN, Epi>;
+  using Smem = GemmSmem<kBN, kStages, CG>;
+  auto kern = gemm_sm100_kernel<kBN, kStages, CG, A_MN, B_MN, Epi>;
   static bool configured = false;
   if (!configured) {
     TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      Smem::kBytes));
+    if (CG > 1)
+      TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     configured = true;
   }
   if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
-  const int grid = s.n_units < num_sms() ? s.n_units : num_sms();
-  kern<<<grid, kGemmThreads, Smem::kBytes, st>>>(ma, mb, s, ep);
-  TL_LAUNCH_CHECK();
+  TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
+  const int max_groups = num_sms() / CG;
+  const int groups = s.n_units < max_groups ? s.n_units : max_groups;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(groups * CG);
+  lc.blockDim = dim3(kGemmThreads);
+  lc.dynamicSmemBytes = Smem::kBytes;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TL_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, s, ep));
   count_launch();
   return TL_OK;
 }
@@ -123,8 +148,10 @@ __device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&
       *reinterpret_cast<uint4*>(dst + j) = v;
     }
   } else {
-    for (int j = 0; j < nvalid; ++j)
-      dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(__uint_as_float(r[j]), 0.f) & 0xFFFFu);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)  // static indexing keeps r[] in registers
+      if (j < nvalid)
+        dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(__uint_as_float(r[j]), 0.f) & 0xFFFFu);
   }
 }
 
@@ -456,7 +483,7 @@ ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool
 GemmShape fwd_shape(int rows, int V, int H) {
   const int n_tiles = (V + kBN - 1) / kBN;
   const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
-  return make_shape(rows, V, H, kBN, strip, kGroupM);
+  return make_shape(rows, V, H, kBN, strip, kGroupM, kCG);
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
@@ -465,11 +492,11 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
                          CombineArgs ca, cudaStream_t st, __half_raw* zout = nullptr,
                          long long ldz = 0) {
   CUtensorMap ma, mb;
-  if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
-  if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
+  if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
   const GemmShape s = fwd_shape(rows, V, H);
   EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz};
-  if (int e = launch_gemm<false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD)) return e;
+  if (int e = launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD))
+    return e;
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
@@ -501,26 +528,27 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   TL_REQUIRE(K > 0, TL_ERR_UNSUPPORTED, "K must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUtensorMap ma, mb;
-  if (int e = make_operand_map(&ma, A, a_mn_major != 0, M, K, lda, kBM)) return e;
-  if (int e = make_operand_map(&mb, B, b_mn_major != 0, N, K, ldb, kBN)) return e;
-  const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM);
+  if (int e = make_ab_maps(&ma, &mb, A, a_mn_major != 0, M, lda, B, b_mn_major != 0, N, ldb, K,
+                           kCG))
+    return e;
+  const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
   if (c_fp32) {
     EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
     switch (sel) {
-      case 0: return launch_gemm<false, false, EpiStoreF32>(ma, mb, s, ep, st);
-      case 1: return launch_gemm<false, true, EpiStoreF32>(ma, mb, s, ep, st);
-      case 2: return launch_gemm<true, false, EpiStoreF32>(ma, mb, s, ep, st);
-      default: return launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st);
+      case 0: return launch_gemm<kCG, false, false, EpiStoreF32>(ma, mb, s, ep, st);
+      case 1: return launch_gemm<kCG, false, true, EpiStoreF32>(ma, mb, s, ep, st);
+      case 2: return launch_gemm<kCG, true, false, EpiStoreF32>(ma, mb, s, ep, st);
+      default: return launch_gemm<kCG, true, true, EpiStoreF32>(ma, mb, s, ep, st);
     }
   }
   TL_REQUIRE(!accumulate, TL_ERR_UNSUPPORTED, "accumulate needs fp32 C");
   EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr};
   switch (sel) {
-    case 0: return launch_gemm<false, false, EpiStoreBF16>(ma, mb, s, ep, st);
-    case 1: return launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st);
-    case 2: return launch_gemm<true, false, EpiStoreBF16>(ma, mb, s, ep, st);
-    default: return launch_gemm<true, true, EpiStoreBF16>(ma, mb, s, ep, st);
+    case 0: return launch_gemm<kCG, false, false, EpiStoreBF16>(ma, mb, s, ep, st);
+    case 1: return launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st);
+    case 2: return launch_gemm<kCG, true, false, EpiStoreBF16>(ma, mb, s, ep, st);
+    default: return launch_gemm<kCG, true, true, EpiStoreBF16>(ma, mb, s, ep, st);
   }
 }
 
@@ -649,30 +677,33 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     } else {
       // recompute z -> dS (bf16) in the GEMM epilogue
       CUtensorMap ma, mb;
-      if (int e = make_operand_map(&ma, c.h, false, rows, H, H, kBM)) return e;
-      if (int e = make_operand_map(&mb, weight, false, V, H, H, kBN)) return e;
+      if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG))
+        return e;
       const GemmShape s = fwd_shape(rows, V, H);
       EpiDSoftmax::Params ep{c.y, c.lse, c.g, c.c, c.ez,
                              reinterpret_cast<__nv_bfloat16_raw*>(c.ds), Vld};
-      if (int e = launch_gemm<false, false, EpiDSoftmax>(ma, mb, s, ep, st, PROF_GEMM_DS)) return e;
+      if (int e = launch_gemm<kCG, false, false, EpiDSoftmax>(ma, mb, s, ep, st, PROF_GEMM_DS))
+        return e;
     }
     // dH rows = dS W  -> scattered to packed positions
     {
       CUtensorMap ma, mb;
-      if (int e = make_operand_map(&ma, c.ds, false, rows, V, Vld, kBM)) return e;
-      if (int e = make_operand_map(&mb, weight, true, H, V, H, kBN)) return e;
-      const GemmShape s = make_shape(rows, H, V, kBN, 1, kGroupM);
+      if (int e = make_ab_maps(&ma, &mb, c.ds, false, rows, Vld, weight, true, H, H, V, kCG))
+        return e;
+      const GemmShape s = make_shape(rows, H, V, kBN, 1, kGroupM, kCG);
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
-      if (int e = launch_gemm<false, true, EpiStoreBF16>(ma, mb, s, ep, st, PROF_GEMM_DH)) return e;
+      if (int e = launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st, PROF_GEMM_DH))
+        return e;
     }
     // dW (+)= dS^T h_c
     {
       CUtensorMap ma, mb;
-      if (int e = make_operand_map(&ma, c.ds, true, V, rows, Vld, kBM)) return e;
-      if (int e = make_operand_map(&mb, c.h, true, H, rows, H, kBN)) return e;
-      const GemmShape s = make_shape(V, H, rows, kBN, 1, kGroupM);
+      if (int e = make_ab_maps(&ma, &mb, c.ds, true, V, Vld, c.h, true, H, H, rows, kCG))
+        return e;
+      const GemmShape s = make_shape(V, H, rows, kBN, 1, kGroupM, kCG);
       EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
-      if (int e = launch_gemm<true, true, EpiStoreF32>(ma, mb, s, ep, st, PROF_GEMM_DW)) return e;
+      if (int e = launch_gemm<kCG, true, true, EpiStoreF32>(ma, mb, s, ep, st, PROF_GEMM_DW))
+        return e;
     }
   }
   return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,
