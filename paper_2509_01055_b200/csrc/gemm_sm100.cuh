@@ -49,6 +49,15 @@ struct GemmShape {
   int group_m;    // M-tiles per raster group
   int n_units;
   int cg;         // CTAs per tile (M rows per tile = 128 * cg)
+  int pol_a, pol_b;  // L2 eviction policy of the A / B TMA loads (make_policy)
+  // Wave lockstep (optional): the i-th unit of every CTA(-pair) forms wave i;
+  // within a wave every CTA bumps sync_ctr[i] after each `sync_every`
+  // k-blocks it has issued, and may not start sync step s before all CTAs of
+  // the wave finished step s - sync_window.  Keeps the CTAs that share A / B
+  // tiles within a few k-blocks of each other so the sharing hits L2
+  // (unsynchronised they drift apart and re-read operands from HBM 10-18x).
+  int* sync_ctr;  // [n_waves], zeroed before launch (NULL = off)
+  int sync_every, sync_window;
 };
 
 struct UnitCoord {
@@ -78,12 +87,18 @@ __host__ __device__ inline UnitCoord unit_coord(const GemmShape& s, int u) {
   return c;
 }
 
-inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m, int cg = 1) {
+inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m, int cg = 1,
+                            int pol_a = 0, int pol_b = 0) {
   GemmShape s;
   s.M = M;
   s.N = N;
   s.K = K;
   s.cg = cg;
+  s.pol_a = pol_a;
+  s.pol_b = pol_b;
+  s.sync_ctr = nullptr;
+  s.sync_every = 0;
+  s.sync_window = 0;
   s.m_tiles = (M + kBM * cg - 1) / (kBM * cg);
   s.n_tiles = (N + BN - 1) / BN;
   s.k_blocks = (K + kBK - 1) / kBK;
@@ -94,11 +109,18 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m,
   return s;
 }
 
+// BN = tile width; UMMA instructions are N = min(BN, 256) wide, NSUB of them
+// per k-step side by side in TMEM; accumulators are double-buffered when two
+// tiles fit in TMEM's 512 columns (BN <= 256), single-buffered for BN = 512.
 template <int BN, int STAGES, int CG>
 struct GemmSmem {
+  static constexpr int kUmmaN = BN < 256 ? BN : 256;
+  static constexpr int kNSub = BN / kUmmaN;
+  static constexpr int kNAcc = 2 * BN <= 512 ? 2 : 1;
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBRows = BN / CG;  // B rows staged by each CTA
-  static constexpr int kBBytes = kBRows * kBK * 2;
+  static constexpr int kBRows = kUmmaN / CG;  // B rows staged by each CTA per sub-MMA
+  static constexpr int kBSubBytes = kBRows * kBK * 2;
+  static constexpr int kBBytes = kNSub * kBSubBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
@@ -111,11 +133,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       const __grid_constant__ CUtensorMap map_b, const GemmShape shape,
                       const typename Epi::Params ep) {
   using Smem = GemmSmem<BN, STAGES, CG>;
-  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 512 && (BN <= 256 || BN % 256 == 0), "BN");
   static_assert(CG == 1 || CG == 2, "CG");
   static_assert(Smem::kBRows % 64 == 0, "B half tile must be a multiple of 64 rows");
-  constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  constexpr uint32_t kIdesc = idesc_bf16(kBM * CG, BN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+  constexpr int kNAcc = Smem::kNAcc;
+  constexpr int kUmmaN = Smem::kUmmaN;
+  constexpr uint32_t kCols = kNAcc * BN;
+  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : (kCols <= 64 ? 64 : (kCols <= 128 ? 128 : (kCols <= 256 ? 256 : 512)));
+  constexpr uint32_t kIdesc = idesc_bf16(kBM * CG, kUmmaN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -158,41 +183,69 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
+      const uint64_t pol_a = make_policy(shape.pol_a);
+      const uint64_t pol_b = make_policy(shape.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < shape.n_units; u += n_pairs) {
+      int wave = 0;
+      for (int u = pair; u < shape.n_units; u += n_pairs, ++wave) {
         const UnitCoord uc = unit_coord(shape, u);
         const int m0 = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM;
+        int* ctr = shape.sync_ctr ? shape.sync_ctr + wave : nullptr;
+        const int wave_ctas = CG * min(n_pairs, shape.n_units - wave * n_pairs);
+        int sstep = 0, in_step = 0;
         for (int t = 0; t < uc.n_count; ++t) {
+          // sub-MMA j covers tile columns [j*kUmmaN, (j+1)*kUmmaN); this CTA
+          // stages rows rank*kBRows.. of each (the pair MMA splits B in half)
           const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
           for (int kb = 0; kb < shape.k_blocks; ++kb) {
+            if (ctr && in_step == 0 && sstep >= shape.sync_window) {
+              const int need = wave_ctas * (sstep - shape.sync_window + 1);
+              while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
+            }
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * Smem::kStageBytes;
             uint8_t* sb = sa + Smem::kABytes;
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * Smem::kStageBytes);
             const int k0 = kb * kBK;
-            auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1) {
+            auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, uint64_t pol) {
               if constexpr (CG == 2) tma_load_2d_cg2(m, &full_bar[stage], dst, c0, c1, pol);
               else tma_load_2d(m, &full_bar[stage], dst, c0, c1, pol);
             };
             if constexpr (!A_MN) {
-              load(&map_a, sa, k0, m0);
+              load(&map_a, sa, k0, m0, pol_a);
             } else {
 #pragma unroll
-              for (int j = 0; j < kBM / 64; ++j) load(&map_a, sa + j * 8192, m0 + 64 * j, k0);
+              for (int j = 0; j < kBM / 64; ++j) load(&map_a, sa + j * 8192, m0 + 64 * j, k0, pol_a);
             }
-            if constexpr (!B_MN) {
-              load(&map_b, sb, k0, n0);
-            } else {
 #pragma unroll
-              for (int j = 0; j < Smem::kBRows / 64; ++j) load(&map_b, sb + j * 8192, n0 + 64 * j, k0);
+            for (int js = 0; js < Smem::kNSub; ++js) {
+              uint8_t* sbj = sb + js * Smem::kBSubBytes;
+              const int nj = n0 + js * kUmmaN;
+              if constexpr (!B_MN) {
+                load(&map_b, sbj, k0, nj, pol_b);
+              } else {
+#pragma unroll
+                for (int j = 0; j < Smem::kBRows / 64; ++j)
+                  load(&map_b, sbj + j * 8192, nj + 64 * j, k0, pol_b);
+              }
             }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
+            if (ctr && ++in_step == shape.sync_every) {
+              red_release_gpu_add(ctr, 1);
+              in_step = 0;
+              ++sstep;
+            }
           }
+        }
+        if (ctr) {
+          // a unit shorter than the wave's longest counts as finished for
+          // every step a longer unit can still wait on
+          const int max_steps = (shape.strip * shape.k_blocks + shape.sync_every - 1) / shape.sync_every;
+          if (max_steps > sstep) red_release_gpu_add(ctr, max_steps - sstep);
         }
       }
     }
@@ -218,10 +271,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t da = A_MN ? sw128_desc(sa + kk * 2048, 8192, 1024)
                                        : sw128_desc(sa + kk * 32, 16, 1024);
-              const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
-                                       : sw128_desc(sb + kk * 32, 16, 1024);
-              if constexpr (CG == 2) umma_bf16_cg2(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
-              else umma_bf16(d_tmem, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+#pragma unroll
+              for (int js = 0; js < Smem::kNSub; ++js) {
+                const uint32_t sbj = sb + js * Smem::kBSubBytes;
+                const uint64_t db = B_MN ? sw128_desc(sbj + kk * 2048, 8192, 1024)
+                                         : sw128_desc(sbj + kk * 32, 16, 1024);
+                const uint32_t dj = d_tmem + js * kUmmaN;
+                if constexpr (CG == 2) umma_bf16_cg2(dj, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+                else umma_bf16(dj, da, db, kIdesc, (kb | kk) != 0 ? 1u : 0u);
+              }
             }
             if constexpr (CG == 2) umma_commit_cg2_mc(&empty_bar[stage]);
             else umma_commit(&empty_bar[stage]);
@@ -232,7 +290,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if constexpr (CG == 2) umma_commit_cg2_mc(&tfull_bar[acc]);
           else umma_commit(&tfull_bar[acc]);
-          if (++acc == 2) {
+          if (++acc == kNAcc) {
             acc = 0;
             acc_phase ^= 1;
           }
@@ -261,7 +319,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);
           else mbar_arrive(&tempty_bar[acc]);
         }
-        if (++acc == 2) {
+        if (++acc == kNAcc) {
           acc = 0;
           acc_phase ^= 1;
         }

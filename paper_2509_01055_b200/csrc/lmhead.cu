@@ -32,8 +32,11 @@ namespace {
 
 constexpr int kBN = 256;
 constexpr int kCG = 2;  // 2-CTA (cta_group::2) tiles of 256 x 256
+// dH / dW (long K, light epilogue): 256 x 512 pair tiles (two N=256 UMMAs per
+// k-step, TMEM single-buffered) halve the dS re-reads across N tiles.
+constexpr int kBNWide = 512;
 constexpr int kStages = 6;
-constexpr int kStripsFwd = 9;
+constexpr int kStripsFwd = 6;  // even: a wave covers 2 strips of one M group
 constexpr int kGroupM = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -93,12 +96,13 @@ int make_ab_maps(CUtensorMap* ma, CUtensorMap* mb, const void* A, bool a_mn, lon
   return make_operand_map(mb, B, b_mn, N, K, ldb, kBN / cg);
 }
 
-template <int CG, bool A_MN, bool B_MN, class Epi>
+template <int CG, bool A_MN, bool B_MN, class Epi, int BN = kBN>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
                 const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
   ProfScope prof(prof_cat, st);
-  using Smem = GemmSmem<kBN, kStages, CG>;
-  auto kern = gemm_sm100_kernel<kBN, kStages, CG, A_MN, B_MN, Epi>;
+  constexpr int kSt = BN <= 256 ? kStages : 4;  // 48 KB stages at BN = 512
+  using Smem = GemmSmem<BN, kSt, CG>;
+  auto kern = gemm_sm100_kernel<BN, kSt, CG, A_MN, B_MN, Epi>;
   static bool configured = false;
   if (!configured) {
     TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -456,7 +460,22 @@ struct ChunkWs {
   uint8_t* flags;   // [T]
   double* traj_out; // [B*8]
   double* group_out;// [G*8]
+  int* sync;        // [3 * kSyncWaves] wave-lockstep counters (fwd / dH / dW)
 };
+
+constexpr int kSyncWaves = 4096;
+
+// Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr).
+GemmShape with_sync(GemmShape s, int* ctr, int every, int window) {
+  const int n_pairs = num_sms() / s.cg;
+  const int waves = (s.n_units + n_pairs - 1) / n_pairs;
+  if (ctr && waves <= kSyncWaves && every > 0) {
+    s.sync_ctr = ctr;
+    s.sync_every = every;
+    s.sync_window = window;
+  }
+  return s;
+}
 
 long long vld_of(int vocab) { return (vocab + 7) / 8 * 8; }
 
@@ -477,13 +496,21 @@ ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool
   c.flags = w.take<uint8_t>(T);
   c.traj_out = w.take<double>(static_cast<size_t>(B) * 8);
   c.group_out = w.take<double>(static_cast<size_t>(G) * TL_GROUP_OUT_LEN);
+  c.sync = w.take<int>(4 * kSyncWaves);
   return c;
 }
 
-GemmShape fwd_shape(int rows, int V, int H) {
+// Forward LM-head GEMM shape: A-stationary strips.  A wave of n_pairs units
+// is 2 strips x (n_pairs / 2) M-tiles, so the wave's h_c rows (37 x 256 x H
+// bf16 = 67 MB at C2) stay in L2 (evict_last) across the strip while every
+// W tile is fetched once per wave and shared by the n_pairs / 2 pairs of its
+// strip, kept within 2 tiles of each other by the wave lockstep.
+GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int n_tiles = (V + kBN - 1) / kBN;
   const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
-  return make_shape(rows, V, H, kBN, strip, kGroupM, kCG);
+  const int group_m = num_sms() / kCG / 2;
+  GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, /*pol_a=*/2, /*pol_b=*/0);
+  return with_sync(s, sync, s.k_blocks, 2);
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
@@ -493,7 +520,9 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
                          long long ldz = 0) {
   CUtensorMap ma, mb;
   if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
-  const GemmShape s = fwd_shape(rows, V, H);
+  // fresh wave-lockstep counters for this chunk's GEMMs (fwd / dS / dH / dW)
+  TL_CUDA_TRY(cudaMemsetAsync(c.sync, 0, 4 * kSyncWaves * sizeof(int), st));
+  const GemmShape s = fwd_shape(rows, V, H, c.sync);
   EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz};
   if (int e = launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD))
     return e;
@@ -531,8 +560,18 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   if (int e = make_ab_maps(&ma, &mb, A, a_mn_major != 0, M, lda, B, b_mn_major != 0, N, ldb, K,
                            kCG))
     return e;
-  const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
+  if (c_fp32 && N >= 1024) {  // wide 256 x 512 pair tiles (as the dH / dW GEMMs)
+    const GemmShape s = make_shape(M, N, K, kBNWide, 1, kGroupM, kCG);
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
+    switch (sel) {
+      case 0: return launch_gemm<kCG, false, false, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
+      case 1: return launch_gemm<kCG, false, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
+      case 2: return launch_gemm<kCG, true, false, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
+      default: return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
+    }
+  }
+  const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   if (c_fp32) {
     EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
     switch (sel) {
@@ -679,7 +718,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       CUtensorMap ma, mb;
       if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG))
         return e;
-      const GemmShape s = fwd_shape(rows, V, H);
+      const GemmShape s = fwd_shape(rows, V, H, c.sync + kSyncWaves);
       EpiDSoftmax::Params ep{c.y, c.lse, c.g, c.c, c.ez,
                              reinterpret_cast<__nv_bfloat16_raw*>(c.ds), Vld};
       if (int e = launch_gemm<kCG, false, false, EpiDSoftmax>(ma, mb, s, ep, st, PROF_GEMM_DS))
@@ -690,9 +729,13 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       CUtensorMap ma, mb;
       if (int e = make_ab_maps(&ma, &mb, c.ds, false, rows, Vld, weight, true, H, H, V, kCG))
         return e;
-      const GemmShape s = make_shape(rows, H, V, kBN, 1, kGroupM, kCG);
+      // N-complete raster (group_m = 1): all H tiles of an M tile run together
+      // so each dS k-block is fetched from HBM once; dS streams (evict first).
+      const GemmShape s = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
+                                    c.sync + 2 * kSyncWaves, 16, 4);
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
-      if (int e = launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st, PROF_GEMM_DH))
+      if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, s, ep, st,
+                                                                       PROF_GEMM_DH))
         return e;
     }
     // dW (+)= dS^T h_c
@@ -700,9 +743,11 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       CUtensorMap ma, mb;
       if (int e = make_ab_maps(&ma, &mb, c.ds, true, V, Vld, c.h, true, H, H, rows, kCG))
         return e;
-      const GemmShape s = make_shape(V, H, rows, kBN, 1, kGroupM, kCG);
+      const GemmShape s = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
+                                    c.sync + 3 * kSyncWaves, 16, 4);
       EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
-      if (int e = launch_gemm<kCG, true, true, EpiStoreF32>(ma, mb, s, ep, st, PROF_GEMM_DW))
+      if (int e = launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st,
+                                                                     PROF_GEMM_DW))
         return e;
     }
   }

@@ -85,6 +85,25 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 0 = evict_normal, 1 = evict_first (streamed once), 2 = evict_last (reused)
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+  return kind == 2 ? policy_evict_last() : (kind == 1 ? policy_evict_first() : policy_evict_normal());
+}
+
+// --------------------------------------------------- gpu-scope counters ----
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // ------------------------------------------------------------- clusters ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {

@@ -315,7 +315,8 @@ def test_loss_fp32_masking_invariance_bitwise():
 # ---------------------------------------------------------------- GEMM --
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (304, 520, 200), (1000, 96, 1024), (136, 64, 3584)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (304, 520, 200), (1000, 96, 1024),
+                                   (136, 64, 3584), (520, 1600, 328), (256, 1024, 4096)])
 def test_gemm_vs_torch(a_mn, b_mn, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
