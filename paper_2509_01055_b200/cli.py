@@ -1,0 +1,189 @@
+"""`loss` command — drop-in for `toolloop loss` (toolloop/cli.py:272-345).
+
+    python -m paper_2509_01055_b200.cli loss --episodes E [--logprobs S] [--config C]
+
+Reads the episode log (JSON lines, rollout/episodes.py:132-147) and an
+optional log-prob sidecar (cli.py:255-269), packs every trajectory on the GPU
+(K1), computes group advantages (K2) and the masked clipped objective (K3)
+with the fp64 parity kernels for all task_id groups at once, and prints the
+same JSON report as the reference (objective, clip_fraction, masked_tokens,
+kl, groups, episodes).  Errors exit 1 with the reference's messages
+(GroupTooSmall gets the "--samples" hint, cli.py:329-333).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+from .errors import EpisodeLogError, GroupTooSmall, MaskMismatch
+from .trajectory import ACTION, trajectory_from_dict
+
+_LOSS_KEYS = {"epsilon_clip", "kl_beta", "std_floor"}
+
+
+def read_episodes(path) -> list[dict]:
+    """rollout/episodes.py:132-147 — one record per non-blank line; any defect
+    raises EpisodeLogError citing path:line."""
+    path = Path(path)
+    out = []
+    with path.open("r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            if not line.strip():
+                continue
+            try:
+                data = json.loads(line)
+                traj = trajectory_from_dict(data["trajectory"])
+                timings = data["timings"]
+                if len(timings) != len(traj.segments):
+                    raise ValueError(f"timings has {len(timings)} entries for "
+                                     f"{len(traj.segments)} segments")
+                logps = data.get("action_logprobs")
+                if logps is not None:
+                    logps = [[float(x) for x in row] for row in logps]
+                out.append({"task_id": str(data["task_id"]), "reward": float(data["reward"]),
+                            "trajectory": traj, "action_logprobs": logps})
+            except EpisodeLogError:
+                raise
+            except Exception as exc:
+                raise EpisodeLogError(f"{path}:{lineno}: {exc}") from exc
+    return out
+
+
+def flat_logps(record: dict) -> list[float]:
+    """cli.py:233-252 — per-action-segment rows expanded to per-token logps,
+    0.0 on observation positions."""
+    if record["action_logprobs"] is None:
+        raise MaskMismatch(f"episode {record['task_id']!r} has no action_logprobs; supply --logprobs")
+    flat: list[float] = []
+    rows = iter(record["action_logprobs"])
+    for seg in record["trajectory"].segments:
+        if seg.origin == ACTION:
+            row = next(rows, None)
+            if row is None or len(row) != len(seg.tokens):
+                raise MaskMismatch(f"episode {record['task_id']!r}: action_logprobs do not align "
+                                   f"with action segments")
+            flat.extend(row)
+        else:
+            flat.extend(0.0 for _ in seg.tokens)
+    return flat
+
+
+def read_sidecar(path: Path, count: int) -> list[dict]:
+    """cli.py:255-269."""
+    rows = []
+    for lineno, line in enumerate(path.read_text(encoding="utf-8").splitlines(), start=1):
+        if not line.strip():
+            continue
+        try:
+            data = json.loads(line)
+        except json.JSONDecodeError as exc:
+            raise EpisodeLogError(f"{path}:{lineno}: {exc}")
+        if not isinstance(data, dict) or "logp_new" not in data:
+            raise EpisodeLogError(f"{path}:{lineno}: expected an object with 'logp_new'")
+        rows.append(data)
+    if len(rows) != count:
+        raise MaskMismatch(f"{path}: {len(rows)} sidecar rows for {count} episodes")
+    return rows
+
+
+def load_loss_config(path):
+    from .rl.loss import LossConfig
+
+    if path is None:
+        return LossConfig()
+    import yaml
+
+    data = yaml.safe_load(Path(path).read_text(encoding="utf-8")) or {}
+    sec = data.get("loss", {}) or {}
+    bad = set(sec) - _LOSS_KEYS
+    if bad:
+        raise ValueError(f"unknown loss config keys: {sorted(bad)}")
+    return LossConfig(**sec)
+
+
+def loss_report(episodes_path, logprobs_path=None, config_path=None) -> dict:
+    import torch
+
+    from . import grpo, packing
+    from .packing import segment_table
+
+    cfg = load_loss_config(config_path)
+    records = read_episodes(episodes_path)
+    if not records:
+        raise ValueError(f"{episodes_path}: no episodes")
+    n = len(records)
+    if logprobs_path is not None:
+        side = read_sidecar(Path(logprobs_path), n)
+        new = [row["logp_new"] for row in side]
+        old = [row.get("logp_old", row["logp_new"]) for row in side]
+        ref = [row.get("logp_ref") for row in side]
+    else:
+        new = [flat_logps(r) for r in records]
+        old = [list(x) for x in new]
+        ref = [None] * n
+    # token_records' length checks (loss.py:85-90)
+    lens = [sum(len(s.tokens) for s in r["trajectory"].segments) for r in records]
+    for i, (r, L) in enumerate(zip(records, lens)):
+        if not (len(new[i]) == len(old[i]) == L):
+            raise MaskMismatch(f"{L} tokens vs {len(new[i])} new / {len(old[i])} old logps")
+        if ref[i] is not None and len(ref[i]) != L:
+            raise MaskMismatch(f"{L} tokens vs {len(ref[i])} ref logps")
+    # group by task_id in first-appearance order (cli.py:309-311)
+    order: dict[str, list[int]] = {}
+    for i, r in enumerate(records):
+        order.setdefault(r["task_id"], []).append(i)
+    for tid, idxs in order.items():
+        if len(idxs) < 2:
+            raise GroupTooSmall(f"need at least 2 rewards, got {len(idxs)}")
+    perm = [i for idxs in order.values() for i in idxs]
+    group_off = np.zeros(len(order) + 1, dtype=np.int32)
+    group_off[1:] = np.cumsum([len(v) for v in order.values()])
+    table = segment_table([records[i]["trajectory"] for i in perm])
+    packed = packing.pack_table(table)
+    cat = lambda rows: np.concatenate([np.asarray(rows[i], dtype=np.float64) for i in perm]) \
+        if perm else np.zeros(0)  # noqa: E731
+    has_ref = any(x is not None for x in ref)
+    d = lambda a: torch.from_numpy(a if len(a) else np.zeros(1)).cuda()  # noqa: E731
+    lref = None
+    if has_ref:
+        lref = d(np.concatenate([np.asarray(ref[i], dtype=np.float64) if ref[i] is not None
+                                 else np.full(lens[i], math.nan) for i in perm]))
+    rewards = np.asarray([records[i]["reward"] for i in perm], dtype=np.float64)
+    rep = grpo.report_f64(packed, group_off, rewards, d(cat(new)), d(cat(old)), lref, cfg)
+    return {"objective": rep["objective"], "clip_fraction": rep["clip_fraction"],
+            "masked_tokens": rep["masked_tokens"], "kl": rep["kl"], "groups": rep["groups"],
+            "episodes": rep["episodes"]}
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="toolloop-b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    lp = sub.add_parser("loss", help="masked clipped objective over an episode log; print JSON")
+    lp.add_argument("--episodes", required=True)
+    lp.add_argument("--logprobs", default=None)
+    lp.add_argument("--config", default=None)
+    args = ap.parse_args(argv)
+    if not Path(args.episodes).is_file():
+        print(f"Error: episodes file {args.episodes!r} does not exist", file=sys.stderr)
+        return 2
+    try:
+        report = loss_report(args.episodes, args.logprobs, args.config)
+    except GroupTooSmall as exc:
+        print(f"Error: {exc}; groups need at least 2 episodes per task_id "
+              f"(roll out with --samples 2 or more)")
+        return 1
+    except (MaskMismatch, EpisodeLogError, ValueError) as exc:
+        print(f"Error: {exc}")
+        return 1
+    print(json.dumps(report, indent=2))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -465,8 +465,17 @@ struct ChunkWs {
 
 constexpr int kSyncWaves = 4096;
 
+// Tuning overrides (profiling only): TL_SYNC_<name>=every,window ; every=0 disables.
+void sync_override(const char* name, int& every, int& window) {
+  char key[64];
+  snprintf(key, sizeof(key), "TL_SYNC_%s", name);
+  const char* v = getenv(key);
+  if (v) sscanf(v, "%d,%d", &every, &window);
+}
+
 // Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr).
-GemmShape with_sync(GemmShape s, int* ctr, int every, int window) {
+GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* name = nullptr) {
+  if (name) sync_override(name, every, window);
   const int n_pairs = num_sms() / s.cg;
   const int waves = (s.n_units + n_pairs - 1) / n_pairs;
   if (ctr && waves <= kSyncWaves && every > 0) {
@@ -510,7 +519,7 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
   const int group_m = num_sms() / kCG / 2;
   GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, /*pol_a=*/2, /*pol_b=*/0);
-  return with_sync(s, sync, s.k_blocks, 2);
+  return with_sync(s, sync, s.k_blocks, 2, "FWD");
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
@@ -732,7 +741,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       // N-complete raster (group_m = 1): all H tiles of an M tile run together
       // so each dS k-block is fetched from HBM once; dS streams (evict first).
       const GemmShape s = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
-                                    c.sync + 2 * kSyncWaves, 16, 4);
+                                    c.sync + 2 * kSyncWaves, 8, 2, "DH");
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, s, ep, st,
                                                                        PROF_GEMM_DH))
@@ -744,7 +753,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       if (int e = make_ab_maps(&ma, &mb, c.ds, true, V, Vld, c.h, true, H, H, rows, kCG))
         return e;
       const GemmShape s = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
-                                    c.sync + 3 * kSyncWaves, 16, 4);
+                                    c.sync + 3 * kSyncWaves, 8, 2, "DW");
       EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
       if (int e = launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st,
                                                                      PROF_GEMM_DW))

@@ -223,6 +223,36 @@ def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_
     return report_dict(rep.cpu()), (grad[:T] if want_grad else None)
 
 
+def report_f64(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_ref=None,
+               cfg: LossConfig | None = None, stream=None) -> dict:
+    """cli.loss's report (cli.py:309-345) for a whole packed batch in the fp64
+    parity kernels: K2 advantages per group, K3 per group in reference order,
+    then the reference aggregation.  logp_* are float64 device tensors [T]
+    (logp_ref may hold NaN where a token has no reference)."""
+    import torch
+
+    L = _lib.lib()
+    cfg = cfg or LossConfig()
+    dev = packed.cu_seqlens.device
+    go = np.asarray(group_off, dtype=np.int32)
+    n_groups = len(go) - 1
+    adv64, _, _, _, d_go = advantages(rewards, go, std_floor=cfg.std_floor, device=dev,
+                                      stream=stream)
+    T = packed.n_tokens
+    ws_bytes = int(L.tl_loss_f64_workspace_bytes(max(T, 1)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    gout = torch.empty(max(n_groups, 1) * _lib.TL_GROUP_OUT_LEN, dtype=torch.float64, device=dev)
+    rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
+    c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
+    s = _lib.stream_handle(stream)
+    _lib.check(L.tl_loss_f64(logp_new.data_ptr(), logp_old.data_ptr(), _lib.ptr(logp_ref),
+                             packed.loss_mask.data_ptr(), packed.cu_seqlens.data_ptr(),
+                             d_go.data_ptr(), adv64.data_ptr(), packed.n_traj, n_groups, T, c,
+                             None, gout.data_ptr(), ws.data_ptr(), ws_bytes, s))
+    _lib.check(L.tl_report_f64(gout.data_ptr(), n_groups, packed.n_traj, rep.data_ptr(), s))
+    return report_dict(rep.cpu())
+
+
 def lmhead_logprobs(hidden, weight, targets, rows=None, *, chunk_rows: int | None = None,
                     stream=None):
     """Forward-only fused LM head (F3: rollout-side logp_old / logp_ref).
