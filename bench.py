@@ -393,11 +393,21 @@ def main():
     gemm_ms = sum(prof.get(k, (0, 0))[0] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     gemm_launch = sum(prof.get(k, (0, 0))[1] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     roofline = None
+    traffic, traffic_note = None, None
+    tp = ROOT / "profiles" / "r1_gemm_traffic.json"
+    if tp.exists() and cfg.name == "c2":
+        tj = json.loads(tp.read_text())
+        per_chunk = sum(v["dram_read_GB"] + v["dram_write_GB"]
+                        for k, v in tj["per_chunk"].items() if k.startswith("gemm"))
+        traffic = per_chunk * 1e9 * wl.n_act / tj["chunk_rows"]
+        traffic_note = (f"bytes/step = ncu --set full DRAM read+write of the fwd/dH/dW GEMM launches "
+                        f"of one {tj['chunk_rows']}-row chunk ({per_chunk:.1f} GB, {tp.name}) x chunks/step; "
+                        f"per chunk each GEMM must read W (1.09 GB) and h_c or dS (0.27 / 11.5 GB) once")
     if gemm_ms > 0:
         ach = flops_alg / (gemm_ms / 1e3) / 1e12
         roofline = {
             "bound": "tensor", "achieved": ach, "peak": peak_s, "unit": "TFLOP/s",
-            "frac": ach / peak_s, "traffic": None,
+            "frac": ach / peak_s, "traffic": traffic, "traffic_note": traffic_note,
             "kernel": "gemm_sm100_kernel (tcgen05 LM-head fwd / dS recompute / dH / dW), "
                       "algorithmic 6*T_act*H*V per step over their summed event time",
             "launches_per_step": gemm_launch,
