@@ -247,6 +247,25 @@ def clipped_grad(trajs, advs, eps: float = 0.2, beta: float = 0.0, eps_high: flo
     return grads
 
 
+def term_and_grad(new, old, ref, a, eps: float = 0.2, beta: float = 0.0,
+                  eps_high: float | None = None):
+    """One action token's A11 term (loss.py:179-190) and d term / d logp_new
+    (clipped-arm restatement, as clipped_grad without the 1/(n_i G) scale)."""
+    lo = 1.0 - eps
+    hi = 1.0 + (eps if eps_high is None else eps_high)
+    d = new - old
+    r = token_ratio(new, old)
+    ua, ca = r * a, min(max(r, lo), hi) * a
+    term = min(ua, ca)
+    g = r * a if (not (d > CLAMP or d < -CLAMP) and ua <= ca) else 0.0
+    if ref is not None:
+        term -= beta * k3(ref, new)
+        e = ref - new
+        if -CLAMP <= e <= CLAMP:
+            g += beta * (math.exp(e) - 1.0)
+    return term, g
+
+
 def token_mean(trajs_by_group, advs_by_group, eps: float = 0.2, beta: float = 0.0,
                eps_high: float | None = None):
     """DAPO token-mean aggregation (build extension, parity unpinned; SPEC.md:500

@@ -194,14 +194,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int* ctr = shape.sync_ctr ? shape.sync_ctr + wave : nullptr;
         const int wave_ctas = CG * min(n_pairs, shape.n_units - wave * n_pairs);
         int sstep = 0, in_step = 0;
+        bool do_wait = true;
         for (int t = 0; t < uc.n_count; ++t) {
           // sub-MMA j covers tile columns [j*kUmmaN, (j+1)*kUmmaN); this CTA
           // stages rows rank*kBRows.. of each (the pair MMA splits B in half)
           const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
           for (int kb = 0; kb < shape.k_blocks; ++kb) {
-            if (ctr && in_step == 0 && sstep >= shape.sync_window) {
+            if (ctr && do_wait && in_step == 0 && sstep >= shape.sync_window) {
+              // The lockstep only shapes L2 reuse, never correctness: a wait that
+              // exceeds ~50 ms (co-residency lost, preemption) stops waiting for
+              // the rest of this wave instead of hanging (progress is still
+              // published so the other CTAs are not held up either).
               const int need = wave_ctas * (sstep - shape.sync_window + 1);
-              while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
+              int spins = 0;
+              while (ld_acquire_gpu(ctr) < need) {
+                __nanosleep(64);
+                if (++spins > (1 << 19)) {
+                  do_wait = false;
+                  break;
+                }
+              }
             }
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * Smem::kStageBytes;

@@ -103,20 +103,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   constexpr int kSt = BN <= 256 ? kStages : 4;  // 48 KB stages at BN = 512
   using Smem = GemmSmem<BN, kSt, CG>;
   auto kern = gemm_sm100_kernel<BN, kSt, CG, A_MN, B_MN, Epi>;
-  static bool configured = false;
-  if (!configured) {
-    TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Smem::kBytes));
-    if (CG > 1)
-      TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    configured = true;
-  }
-  if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
-  TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
-  const int max_groups = num_sms() / CG;
-  const int groups = s.n_units < max_groups ? s.n_units : max_groups;
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(groups * CG);
   lc.blockDim = dim3(kGemmThreads);
   lc.dynamicSmemBytes = Smem::kBytes;
   lc.stream = st;
@@ -127,6 +114,24 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  // Persistent grid: never more CTA groups than can be co-resident (the
+  // wave lockstep and the static unit schedule assume every group is live).
+  static int max_groups = 0;
+  if (max_groups == 0) {
+    TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Smem::kBytes));
+    lc.gridDim = dim3(num_sms());
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0) {
+      cudaGetLastError();
+      active = num_sms() / CG;
+    }
+    max_groups = active < num_sms() / CG ? active : num_sms() / CG;
+  }
+  if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
+  TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
+  const int groups = s.n_units < max_groups ? s.n_units : max_groups;
+  lc.gridDim = dim3(groups * CG);
   TL_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, s, ep));
   count_launch();
   return TL_OK;

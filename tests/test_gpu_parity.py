@@ -411,3 +411,45 @@ def test_grpo_lmhead_step_vs_oracle(H, V, chunk, recompute):
     assert _rel_fro(got_dh[act], dH) <= 2e-2
     assert np.all(got_dh[packed.loss_mask.cpu().numpy() == 0] == 0)
     assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
+
+
+def test_grpo_lmhead_step_dapo_token_mean():
+    """DAPO token-mean + clip-higher through the fused step (parity unpinned:
+    oracle restatement)."""
+    from oracle import lmhead_oracle as LH
+
+    H, V = 128, 1000
+    trajs, rewards, go, _, lold, _ = _synthetic_batch(6, n_groups=5, G=4, with_ref=False)
+    for tr in trajs:
+        for i, (o, toks) in enumerate(tr):
+            tr[i] = (o, [t % V for t in toks])
+    packed = packing.pack([_traj(s) for s in trajs])
+    T = packed.n_tokens
+    g = torch.Generator(device="cuda").manual_seed(5)
+    h = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
+    ids = packed.input_ids.cpu().numpy()
+    act = packed.act_idx.cpu().numpy()
+    hn, Wn = _bf16_np(h), _bf16_np(W)
+    lp, _, _ = LH.lmhead_forward(hn[act], Wn, ids[act])
+    lo = lold.copy()
+    lo[act] = lp + np.random.default_rng(1).normal(0, 0.2, len(act))   # ratios around 1
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    cfg = L.LossConfig(epsilon_clip=0.2, eps_high=0.28, loss_agg="token-mean")
+    res = grpo.GRPOStep(H, V, cfg)(packed, go, rewards, h, W, f(lo))
+    torch.cuda.synchronize()
+    lo32 = lo.astype(np.float32).astype(np.float64)
+    adv = np.zeros(len(trajs))
+    for gi in range(len(go) - 1):
+        adv[go[gi]:go[gi + 1]] = O.group_advantages(rewards[go[gi]:go[gi + 1]].tolist())
+    tot = packed.traj_of_token.cpu().numpy()
+    terms, grads = [], np.zeros(T)
+    for k, p in enumerate(act):
+        t, gr = O.term_and_grad(lp[k], lo32[p], None, adv[tot[p]], 0.2, 0.0, 0.28)
+        terms.append(t)
+        grads[p] = gr
+    obj = sum(terms) / len(act)
+    assert abs(res.report["objective"] - obj) <= 1e-4
+    dH, dW = LH.lmhead_backward(hn[act], Wn, ids[act], -grads[act] / len(act))
+    assert _rel_fro(res.dhidden.float().cpu().numpy()[act], dH) <= 2e-2
+    assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
