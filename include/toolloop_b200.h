@@ -36,7 +36,8 @@ typedef enum tl_status {
   TL_ERR_GROUP_TOO_SMALL = 3, /* errors.GroupTooSmall (errors.py:32)           */
   TL_ERR_CUDA = 4,
   TL_ERR_UNSUPPORTED = 5,
-  TL_ERR_WORKSPACE = 6
+  TL_ERR_WORKSPACE = 6,
+  TL_ERR_EPISODE_LOG = 7      /* errors.EpisodeLogError (errors.py:44), "path:line: ..." */
 } tl_status;
 
 const char* tl_last_error(void);
@@ -198,6 +199,28 @@ int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const in
                         uint16_t* dhidden, float* dweight, double* report, int32_t chunk_rows,
                         int32_t mode, void* workspace, size_t workspace_bytes,
                         tl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * F1 — episode-log / sidecar ingest (host, multithreaded C++).
+ * Replaces rollout/episodes.read_episodes (episodes.py:132-147) +
+ * EpisodeRecord.from_dict (:95-120) + trajectory_from_dict
+ * (trajectory.py:182-200), cli._read_sidecar (cli.py:255-269),
+ * cli._flat_logps (cli.py:233-252) and the task_id grouping of cli.loss
+ * (cli.py:309-311).  Produces the SoA segment table of tl_pack_varlen with
+ * episodes permuted so each task_id group (first-appearance order) is
+ * contiguous, plus per-token fp64 log-probs (logp_ref NaN where a sidecar row
+ * has none).  sidecar_path NULL = log-probs embedded in the episode log
+ * (logp_old := logp_new, observation positions 0.0).
+ * ---------------------------------------------------------------------- */
+typedef struct tl_episode_batch tl_episode_batch;
+int tl_ingest_open(const char* episodes_path, const char* sidecar_path, tl_episode_batch** out);
+int tl_ingest_sizes(const tl_episode_batch* batch, int64_t* n_episodes, int64_t* n_segments,
+                    int64_t* n_tokens, int64_t* n_groups, int32_t* has_ref);
+int tl_ingest_fill(const tl_episode_batch* batch, int32_t* token_pool, int32_t* seg_src_off,
+                   int32_t* seg_len, uint8_t* seg_is_action, int32_t* traj_seg_off,
+                   int32_t* group_off, double* rewards, double* logp_new, double* logp_old,
+                   double* logp_ref);
+void tl_ingest_free(tl_episode_batch* batch);
 
 /* Plain tcgen05 GEMM (building block, exported for tests):
  * C[M,N] (+)= A[M,K] * B[N,K]^T with A given K-major ([M,K], lda) or MN-major

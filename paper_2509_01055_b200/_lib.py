@@ -22,6 +22,7 @@ TL_ERR_GROUP_TOO_SMALL = 3
 TL_ERR_CUDA = 4
 TL_ERR_UNSUPPORTED = 5
 TL_ERR_WORKSPACE = 6
+TL_ERR_EPISODE_LOG = 7
 TL_GROUP_OUT_LEN = 8
 TL_REPORT_LEN = 12
 
@@ -35,6 +36,7 @@ EXPORTS = [
     "tl_loss_f32_workspace_bytes", "tl_loss_f32",
     "tl_lmhead_workspace_bytes", "tl_lmhead_logprobs", "tl_grpo_lmhead_step",
     "tl_gemm_bf16",
+    "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
 ]
 
 
@@ -81,6 +83,11 @@ _SIGS = {
                                       _P, _P, _I32, _I32, _P, _SZ, _P]),
     "tl_gemm_bf16": (C.c_int, [_P, _I32, _I64, _P, _I32, _I64, _I32, _I32, _I32, _P, _I32, _I64,
                                _I32, _P]),
+    "tl_ingest_open": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "tl_ingest_sizes": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
+                                  C.POINTER(_I64), C.POINTER(_I32)]),
+    "tl_ingest_fill": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "tl_ingest_free": (None, [_P]),
 }
 
 _lock = threading.Lock()
@@ -124,6 +131,10 @@ def check(status: int) -> None:
         raise GroupTooSmall(msg)
     if status == TL_ERR_INVALID_ARG:
         raise ValueError(msg)
+    if status == TL_ERR_EPISODE_LOG:
+        from .errors import EpisodeLogError
+
+        raise EpisodeLogError(msg)
     raise ToolloopError(f"toolloop-b200 status {status}: {msg}")
 
 

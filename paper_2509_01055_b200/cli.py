@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import sys
 from pathlib import Path
 
@@ -108,54 +107,22 @@ def load_loss_config(path):
 
 
 def loss_report(episodes_path, logprobs_path=None, config_path=None) -> dict:
+    """Episode log (+ sidecar) -> native ingest (F1, C++) -> K1 pack -> K2
+    advantages -> K3 fp64 loss -> cli.loss report."""
     import torch
 
     from . import grpo, packing
-    from .packing import segment_table
+    from .ingest import ingest
 
     cfg = load_loss_config(config_path)
-    records = read_episodes(episodes_path)
-    if not records:
-        raise ValueError(f"{episodes_path}: no episodes")
-    n = len(records)
-    if logprobs_path is not None:
-        side = read_sidecar(Path(logprobs_path), n)
-        new = [row["logp_new"] for row in side]
-        old = [row.get("logp_old", row["logp_new"]) for row in side]
-        ref = [row.get("logp_ref") for row in side]
-    else:
-        new = [flat_logps(r) for r in records]
-        old = [list(x) for x in new]
-        ref = [None] * n
-    # token_records' length checks (loss.py:85-90)
-    lens = [sum(len(s.tokens) for s in r["trajectory"].segments) for r in records]
-    for i, (r, L) in enumerate(zip(records, lens)):
-        if not (len(new[i]) == len(old[i]) == L):
-            raise MaskMismatch(f"{L} tokens vs {len(new[i])} new / {len(old[i])} old logps")
-        if ref[i] is not None and len(ref[i]) != L:
-            raise MaskMismatch(f"{L} tokens vs {len(ref[i])} ref logps")
-    # group by task_id in first-appearance order (cli.py:309-311)
-    order: dict[str, list[int]] = {}
-    for i, r in enumerate(records):
-        order.setdefault(r["task_id"], []).append(i)
-    for tid, idxs in order.items():
-        if len(idxs) < 2:
-            raise GroupTooSmall(f"need at least 2 rewards, got {len(idxs)}")
-    perm = [i for idxs in order.values() for i in idxs]
-    group_off = np.zeros(len(order) + 1, dtype=np.int32)
-    group_off[1:] = np.cumsum([len(v) for v in order.values()])
-    table = segment_table([records[i]["trajectory"] for i in perm])
-    packed = packing.pack_table(table)
-    cat = lambda rows: np.concatenate([np.asarray(rows[i], dtype=np.float64) for i in perm]) \
-        if perm else np.zeros(0)  # noqa: E731
-    has_ref = any(x is not None for x in ref)
-    d = lambda a: torch.from_numpy(a if len(a) else np.zeros(1)).cuda()  # noqa: E731
-    lref = None
-    if has_ref:
-        lref = d(np.concatenate([np.asarray(ref[i], dtype=np.float64) if ref[i] is not None
-                                 else np.full(lens[i], math.nan) for i in perm]))
-    rewards = np.asarray([records[i]["reward"] for i in perm], dtype=np.float64)
-    rep = grpo.report_f64(packed, group_off, rewards, d(cat(new)), d(cat(old)), lref, cfg)
+    b = ingest(episodes_path, logprobs_path, pinned=True)
+    sizes = np.diff(b.group_off)
+    if np.any(sizes < 2):
+        raise GroupTooSmall(f"need at least 2 rewards, got {int(sizes[np.argmax(sizes < 2)])}")
+    packed = packing.pack_table(b.table)
+    d = lambda a: torch.from_numpy(a if len(a) else np.zeros(1)).to("cuda", non_blocking=True)  # noqa: E731
+    lref = None if b.logp_ref is None else d(b.logp_ref)
+    rep = grpo.report_f64(packed, b.group_off, b.rewards, d(b.logp_new), d(b.logp_old), lref, cfg)
     return {"objective": rep["objective"], "clip_fraction": rep["clip_fraction"],
             "masked_tokens": rep["masked_tokens"], "kl": rep["kl"], "groups": rep["groups"],
             "episodes": rep["episodes"]}

@@ -1,0 +1,123 @@
+"""Native ingest (csrc/ingest.cpp) vs the Python restatement of the
+reference's read_episodes / _read_sidecar / _flat_logps / task_id grouping,
+on the reference-generated episode log.  Host-only: runs on CPU."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from paper_2509_01055_b200 import cli
+from paper_2509_01055_b200.errors import EpisodeLogError, MaskMismatch
+from paper_2509_01055_b200.ingest import ingest
+from paper_2509_01055_b200.packing import segment_table
+
+
+def _files(tmp_path, golden_cli):
+    ep = tmp_path / "ep.jsonl"
+    ep.write_text(golden_cli["episodes_jsonl"], encoding="utf-8")
+    sc = tmp_path / "sc.jsonl"
+    sc.write_text("".join(json.dumps(r) + "\n" for r in golden_cli["sidecar"]), encoding="utf-8")
+    return ep, sc
+
+
+def _python_path(ep, sc=None):
+    recs = cli.read_episodes(ep)
+    order = {}
+    for i, r in enumerate(recs):
+        order.setdefault(r["task_id"], []).append(i)
+    perm = [i for v in order.values() for i in v]
+    tab = segment_table([recs[i]["trajectory"] for i in perm])
+    if sc is None:
+        new = [cli.flat_logps(recs[i]) for i in perm]
+        old, ref = new, None
+    else:
+        side = cli.read_sidecar(sc, len(recs))
+        new = [side[i]["logp_new"] for i in perm]
+        old = [side[i].get("logp_old", side[i]["logp_new"]) for i in perm]
+        ref = [side[i].get("logp_ref") for i in perm]
+    go = np.cumsum([0] + [len(v) for v in order.values()])
+    return tab, go, [recs[i]["reward"] for i in perm], new, old, ref
+
+
+@pytest.mark.parametrize("with_sidecar", [False, True])
+def test_ingest_matches_python(tmp_path, golden_cli, with_sidecar):
+    ep, sc = _files(tmp_path, golden_cli)
+    b = ingest(ep, sc if with_sidecar else None)
+    tab, go, rw, new, old, ref = _python_path(ep, sc if with_sidecar else None)
+    assert np.array_equal(b.group_off, go)
+    assert b.rewards.tolist() == rw
+    # same packed ids / mask after flatten (pool layout may differ; compare flattened)
+    def flat(t):
+        ids, mask = [], []
+        for s in range(t.n_seg):
+            o, n = t.seg_src_off[s], t.seg_len[s]
+            ids += t.token_pool[o:o + n].tolist()
+            mask += [int(t.seg_is_action[s])] * int(n)
+        return ids, mask
+    assert flat(b.table) == flat(tab)
+    assert np.array_equal(b.table.traj_seg_off, tab.traj_seg_off)
+    assert b.logp_new.tolist() == [x for row in new for x in row]
+    assert b.logp_old.tolist() == [x for row in old for x in row]
+    if with_sidecar:
+        exp = [x for row in ref for x in row]
+        assert all((a == e) for a, e in zip(b.logp_ref.tolist(), exp))
+    else:
+        assert b.logp_ref is None
+
+
+def test_ingest_corrupted_line(tmp_path, golden_cli):
+    ep, _ = _files(tmp_path, golden_cli)
+    n = len([l for l in golden_cli["episodes_jsonl"].splitlines() if l.strip()])
+    with ep.open("a") as fh:
+        fh.write("\n{broken\n")
+    with pytest.raises(EpisodeLogError, match=f":{n + 2}:"):
+        ingest(ep)
+
+
+def test_ingest_validation_errors(tmp_path, golden_cli):
+    lines = golden_cli["episodes_jsonl"].splitlines()
+    rec = json.loads(lines[0])
+    bad = dict(rec)
+    bad["trajectory"] = dict(rec["trajectory"], turn_count=99)
+    p = tmp_path / "bad.jsonl"
+    p.write_text(json.dumps(bad) + "\n")
+    with pytest.raises(EpisodeLogError, match=":1: turn_count"):
+        ingest(p)
+    bad = dict(rec)
+    bad["trajectory"] = dict(rec["trajectory"], segments=rec["trajectory"]["segments"][1:])
+    p.write_text(json.dumps(bad) + "\n")
+    with pytest.raises(EpisodeLogError):
+        ingest(p)
+    bad = dict(rec)
+    del bad["reward"]
+    p.write_text(json.dumps(bad) + "\n")
+    with pytest.raises(EpisodeLogError, match="reward"):
+        ingest(p)
+
+
+def test_ingest_sidecar_mismatches(tmp_path, golden_cli):
+    ep, sc = _files(tmp_path, golden_cli)
+    short = tmp_path / "short.jsonl"
+    short.write_text(json.dumps({"logp_new": [0.0]}) + "\n")
+    with pytest.raises(MaskMismatch):
+        ingest(ep, short)
+    rows = [dict(r) for r in golden_cli["sidecar"]]
+    rows[3]["logp_new"] = rows[3]["logp_new"][:-1]
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text("".join(json.dumps(r) + "\n" for r in rows))
+    with pytest.raises(MaskMismatch):
+        ingest(ep, bad)
+
+
+def test_ingest_escapes_and_nonfinite(tmp_path, golden_cli):
+    rec = json.loads(golden_cli["episodes_jsonl"].splitlines()[0])
+    rec["task_id"] = "t\u00e9\"\\x\U0001F600"
+    rec["trajectory"]["segments"][0]["text"] = "a\nb\t\u2603"
+    rec2 = dict(rec)
+    p = tmp_path / "e.jsonl"
+    p.write_text(json.dumps(rec) + "\n" + json.dumps(rec2) + "\n", encoding="utf-8")
+    b = ingest(p)
+    assert b.n_episodes == 2 and b.group_off.tolist() == [0, 2]
+    assert math.isfinite(b.logp_new.sum())
