@@ -13,6 +13,7 @@
 // in line order and episodes are permuted so every task_id group is
 // contiguous, ready for tl_pack_varlen / tl_group_advantages / tl_loss_f64.
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -152,10 +153,10 @@ struct Reader {
     while (p < end && ((*p >= '0' && *p <= '9') || *p == '.' || *p == 'e' || *p == 'E' ||
                        *p == '+' || *p == '-'))
       ++p;
-    std::string tmp(s, p);
-    char* e = nullptr;
-    double v = strtod(tmp.c_str(), &e);
-    if (e != tmp.c_str() + tmp.size()) fail("bad number");
+    // std::from_chars: correctly rounded like CPython's float(), no allocation
+    double v = 0.0;
+    const auto r = std::from_chars(s, p, v);
+    if (r.ec != std::errc() || r.ptr != p) fail("bad number");
     return v;
   }
   bool is_null() {
@@ -485,8 +486,9 @@ bool parse_parallel(const std::vector<Line>& lines, std::vector<T>& out, F&& fn,
                     int& err_line) {
   const size_t n = lines.size();
   out.resize(n);
+  // episodes are long lines (thousands of numbers): one thread per line is fine
   unsigned nt = std::thread::hardware_concurrency();
-  nt = std::max(1u, std::min(nt, static_cast<unsigned>((n + 255) / 256)));
+  nt = std::max(1u, std::min(nt, static_cast<unsigned>(n)));
   std::vector<std::string> errs(nt);
   std::vector<int> eline(nt, 0);
   std::vector<std::thread> th;

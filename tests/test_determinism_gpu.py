@@ -1,0 +1,47 @@
+"""Run-to-run determinism of the fused step (race detection /
+deterministic reductions): two identical GRPO steps must agree bitwise in
+every output — no float atomics anywhere on the path."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2509_01055_b200 import grpo, packing  # noqa: E402
+from paper_2509_01055_b200.rl.loss import LossConfig  # noqa: E402
+from paper_2509_01055_b200.synthetic import CONFIGS, make_workload  # noqa: E402
+
+
+@pytest.mark.parametrize("recompute", [False, True])
+def test_step_bitwise_deterministic(recompute):
+    cfg = CONFIGS["tiny"]
+    wl = make_workload(cfg)
+    H, V = cfg.hidden, cfg.vocab
+    packed = packing.pack_table(wl.table)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    h = torch.randn((wl.n_tokens, H), device="cuda", generator=g).bfloat16()
+    W = (torch.randn((V, H), device="cuda", generator=g) * 0.05).bfloat16()
+    lold = torch.from_numpy(wl.logp_old).cuda()
+    lref = torch.from_numpy(wl.logp_ref).cuda()
+    step = grpo.GRPOStep(H, V, LossConfig(kl_beta=0.04, entropy_coef=0.01), chunk_rows=256,
+                         recompute=recompute)
+    outs = []
+    for _ in range(2):
+        r = step(packed, wl.group_off, wl.rewards, h, W, lold, lref)
+        outs.append((r.report_tensor.clone(), r.logp.clone(), r.entropy.clone(),
+                     r.dhidden.clone(), r.dweight.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_pack_deterministic_under_arrival_order():
+    wl = make_workload(CONFIGS["tiny"], arrival_order=True)
+    wl2 = make_workload(CONFIGS["tiny"], arrival_order=False)
+    a = packing.pack_table(wl.table)
+    b = packing.pack_table(wl2.table)
+    for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "act_idx"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    assert np.array_equal(a.act_off.cpu().numpy(), b.act_off.cpu().numpy())
