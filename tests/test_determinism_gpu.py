@@ -38,10 +38,15 @@ def test_step_bitwise_deterministic(recompute):
 
 
 def test_pack_deterministic_under_arrival_order():
-    wl = make_workload(CONFIGS["tiny"], arrival_order=True)
-    wl2 = make_workload(CONFIGS["tiny"], arrival_order=False)
-    a = packing.pack_table(wl.table)
-    b = packing.pack_table(wl2.table)
+    """The same segments laid out in arrival order vs segment order pack
+    identically."""
+    t = make_workload(CONFIGS["tiny"], arrival_order=True).table
+    pool = np.concatenate([t.token_pool[o:o + n] for o, n in zip(t.seg_src_off, t.seg_len)])
+    src = np.concatenate([[0], np.cumsum(t.seg_len)[:-1]]).astype(np.int32)
+    t2 = packing.SegmentTable(pool.astype(np.int32), src, t.seg_len, t.seg_is_action,
+                              t.traj_seg_off)
+    a = packing.pack_table(t)
+    b = packing.pack_table(t2)
     for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "act_idx"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
     assert np.array_equal(a.act_off.cpu().numpy(), b.act_off.cpu().numpy())
