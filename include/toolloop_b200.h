@@ -98,6 +98,39 @@ int tl_group_advantages(const double* rewards, const int32_t* group_off, int32_t
                         double norm_groups, double norm_tokens, double* adv64, float* adv32,
                         float* traj_w, int32_t* traj_group, tl_stream_t stream);
 
+/* F2 — verifiable rewards fused into K2.  Replaces the numeric part of
+ * rl/rewards.py:15-68 (string matching stays on the host: `correct` is the
+ * matcher's verdict, or terminated_ok for SWE):
+ *   MATCH  +1 / -1 (:21-23)        MATH  +1 / -1.25 (:26-33)
+ *   DEEPSEARCH  +-1 + 0.1*tool (:36-41)
+ *   VISUAL_REASONER  r_acc + alpha*max(h - RaPR, 0)*invoked + beta*min(n - n_vo, 0)
+ *     with RaPR = invoked responses / G of the group, computed in the warp (:43-63)
+ *   SWE  1 iff terminated_ok and all tests pass (:66-68)
+ * then the group advantages exactly as tl_group_advantages.  Unused signal
+ * arrays may be NULL.  rapr_in [n_groups] (nullable) overrides the computed
+ * RaPR (the reference takes it as an argument); rapr_out [n_groups] nullable. */
+typedef enum tl_reward_kind {
+  TL_REWARD_MATCH = 0,
+  TL_REWARD_MATH = 1,
+  TL_REWARD_DEEPSEARCH = 2,
+  TL_REWARD_VISUAL_REASONER = 3,
+  TL_REWARD_SWE = 4
+} tl_reward_kind;
+typedef struct tl_reward_params {
+  int32_t kind;
+  int32_t n;     /* visual reasoner: free tool calls (default 1)      */
+  double h;      /* visual reasoner: RaPR target (default 0.3)        */
+  double alpha;  /* visual reasoner: curiosity weight (default 0.5)   */
+  double beta;   /* visual reasoner: over-use penalty (default 0.05)  */
+} tl_reward_params;
+int tl_group_rewards_advantages(const tl_reward_params* params, const uint8_t* correct,
+                                const uint8_t* tool_called, const int32_t* n_vo,
+                                const double* r_acc, const uint8_t* tests_pass,
+                                const int32_t* group_off, int32_t n_groups, int32_t n_traj,
+                                double std_floor, const double* rapr_in, double* rewards_out,
+                                double* rapr_out, double* adv64, float* adv32,
+                                tl_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * K3 — masked clipped surrogate (+ diagnostics, + per-token gradient).
  * Replaces rl.loss.grpo_multi_turn_loss (loss.py:150-201, use_mask=1),

@@ -31,7 +31,7 @@ EXPORTS = [
     "tl_last_error", "tl_abi_version", "tl_launch_count",
     "tl_profile_enable", "tl_profile_read", "tl_profile_category",
     "tl_pack_workspace_bytes", "tl_pack_varlen", "tl_pack_padded",
-    "tl_group_advantages",
+    "tl_group_advantages", "tl_group_rewards_advantages",
     "tl_loss_f64_workspace_bytes", "tl_loss_f64", "tl_report_f64", "tl_token_ratio_f64",
     "tl_loss_f32_workspace_bytes", "tl_loss_f32",
     "tl_lmhead_workspace_bytes", "tl_lmhead_logprobs", "tl_grpo_lmhead_step",
@@ -46,6 +46,11 @@ class LossConfigC(C.Structure):
         ("entropy_coef", C.c_double), ("use_mask", C.c_int32), ("has_ref", C.c_int32),
         ("objective", C.c_int32), ("agg", C.c_int32),
     ]
+
+
+class RewardParamsC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("h", C.c_double),
+                ("alpha", C.c_double), ("beta", C.c_double)]
 
 
 _P = C.c_void_p
@@ -67,6 +72,8 @@ _SIGS = {
     "tl_pack_padded": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
     "tl_group_advantages": (C.c_int, [_P, _P, _I32, _I32, _D, _P, _I32, _D, _D, _P, _P, _P, _P,
                                       _P]),
+    "tl_group_rewards_advantages": (C.c_int, [C.POINTER(RewardParamsC), _P, _P, _P, _P, _P, _P,
+                                              _I32, _I32, _D, _P, _P, _P, _P, _P, _P]),
     "tl_loss_f64_workspace_bytes": (_SZ, [_I64]),
     "tl_loss_f64": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I64,
                               C.POINTER(LossConfigC), _P, _P, _P, _SZ, _P]),

@@ -21,12 +21,47 @@ namespace {
 
 constexpr int kAdvWarps = 4;
 
+// F2 — verifiable rewards (rl/rewards.py:15-68) from per-trajectory signals,
+// evaluated inside the advantage warp so the group RaPR (fraction of the
+// group's responses that invoked a tool, rewards.py:43-63) is a warp ballot.
+struct RewardSpec {
+  tl_reward_params p;
+  const uint8_t* correct;      // matcher result / terminated_ok (swe)
+  const uint8_t* tool_called;  // invoked_tool / tool_called
+  const int32_t* n_vo;         // tool invocations (visual reasoner)
+  const double* r_acc;         // accuracy term (visual reasoner)
+  const uint8_t* tests_pass;   // swe
+  double* rewards_out;         // [B]
+  double* rapr_out;            // [n_groups] (nullable)
+  const double* rapr_in;       // [n_groups] override (nullable)
+};
+
+__device__ double reward_of(const RewardSpec& rs, int b, double rapr) {
+  const tl_reward_params& p = rs.p;
+  const bool ok = rs.correct && rs.correct[b];
+  switch (p.kind) {
+    case TL_REWARD_MATCH: return ok ? 1.0 : -1.0;
+    case TL_REWARD_MATH: return ok ? 1.0 : __dadd_rn(-1.0, -0.25);
+    case TL_REWARD_DEEPSEARCH:
+      return __dadd_rn(ok ? 1.0 : -1.0, rs.tool_called[b] ? 0.1 : 0.0);
+    case TL_REWARD_VISUAL_REASONER: {
+      const double gap = __dadd_rn(p.h, -rapr);
+      const double cur = rs.tool_called[b] ? __dmul_rn(p.alpha, 0.0 > gap ? 0.0 : gap) : 0.0;
+      const int over = p.n - rs.n_vo[b];
+      const double pen = __dmul_rn(p.beta, static_cast<double>(over < 0 ? over : 0));
+      return __dadd_rn(__dadd_rn(rs.r_acc[b], cur), pen);
+    }
+    case TL_REWARD_SWE: return (ok && rs.tests_pass[b]) ? 1.0 : 0.0;
+    default: return __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
 __global__ void __launch_bounds__(kAdvWarps * 32)
-    group_adv_kernel(const double* __restrict__ rewards, const int32_t* __restrict__ group_off,
+    group_adv_kernel(const double* rewards, const int32_t* __restrict__ group_off,
                      int n_groups, double std_floor, const int32_t* __restrict__ act_off, int agg,
                      double norm_groups, double norm_tokens, double* __restrict__ adv64,
                      float* __restrict__ adv32, float* __restrict__ traj_w,
-                     int32_t* __restrict__ traj_group) {
+                     int32_t* __restrict__ traj_group, RewardSpec rs) {
   __shared__ long long limbs[kAdvWarps][96];
   __shared__ double bcast[kAdvWarps];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -34,6 +69,25 @@ __global__ void __launch_bounds__(kAdvWarps * 32)
   if (g >= n_groups) return;
   const int b0 = group_off[g], b1 = group_off[g + 1], G = b1 - b0;
   long long* L = limbs[w];
+
+  if (rs.p.kind >= 0) {
+    double rapr = 0.0;
+    if (rs.rapr_in) {
+      rapr = rs.rapr_in[g];
+    } else if (rs.tool_called) {
+      int invoked = 0;
+      for (int i0 = 0; i0 < G; i0 += 32) {
+        const bool t = i0 + lane < G && rs.tool_called[b0 + i0 + lane];
+        invoked += __popc(__ballot_sync(0xffffffffu, t));
+      }
+      rapr = G ? __ddiv_rn(static_cast<double>(invoked), static_cast<double>(G)) : 0.0;
+    }
+    for (int i = lane; i < G; i += 32) rs.rewards_out[b0 + i] = reward_of(rs, b0 + i, rapr);
+    if (rs.rapr_out && lane == 0) rs.rapr_out[g] = rapr;
+    __threadfence_block();
+    __syncwarp();
+    rewards = rs.rewards_out;
+  }
 
   double mean = 0.0, div = 1.0;
   if (G >= 2) {
@@ -102,9 +156,41 @@ extern "C" int tl_group_advantages(const double* rewards, const int32_t* group_o
   if (n_groups == 0) return TL_OK;
   const int grid = (n_groups + tl::kAdvWarps - 1) / tl::kAdvWarps;
   tl::ProfScope prof(tl::PROF_ADV, static_cast<cudaStream_t>(stream));
+  tl::RewardSpec rs{};
+  rs.p.kind = -1;
   tl::group_adv_kernel<<<grid, tl::kAdvWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
       rewards, group_off, n_groups, std_floor, act_off, agg, norm_groups, norm_tokens, adv64,
-      adv32, traj_w, traj_group);
+      adv32, traj_w, traj_group, rs);
+  TL_LAUNCH_CHECK();
+  tl::count_launch();
+  return TL_OK;
+}
+
+extern "C" int tl_group_rewards_advantages(
+    const tl_reward_params* params, const uint8_t* correct, const uint8_t* tool_called,
+    const int32_t* n_vo, const double* r_acc, const uint8_t* tests_pass, const int32_t* group_off,
+    int32_t n_groups, int32_t n_traj, double std_floor, const double* rapr_in,
+    double* rewards_out, double* rapr_out, double* adv64, float* adv32, tl_stream_t stream) {
+  TL_REQUIRE(params && rewards_out, TL_ERR_INVALID_ARG, "params / rewards_out required");
+  TL_REQUIRE(params->kind >= TL_REWARD_MATCH && params->kind <= TL_REWARD_SWE, TL_ERR_INVALID_ARG,
+             "unknown reward kind %d", params->kind);
+  TL_REQUIRE(std_floor > 0.0, TL_ERR_INVALID_ARG, "std_floor must be positive");
+  const int k = params->kind;
+  TL_REQUIRE(k == TL_REWARD_VISUAL_REASONER || correct, TL_ERR_INVALID_ARG, "correct[] required");
+  TL_REQUIRE((k != TL_REWARD_DEEPSEARCH && k != TL_REWARD_VISUAL_REASONER) || tool_called,
+             TL_ERR_INVALID_ARG, "tool_called[] required");
+  TL_REQUIRE(k != TL_REWARD_VISUAL_REASONER || (n_vo && r_acc), TL_ERR_INVALID_ARG,
+             "n_vo[] and r_acc[] required");
+  TL_REQUIRE(k != TL_REWARD_SWE || tests_pass, TL_ERR_INVALID_ARG, "tests_pass[] required");
+  (void)n_traj;
+  if (n_groups == 0) return TL_OK;
+  const int grid = (n_groups + tl::kAdvWarps - 1) / tl::kAdvWarps;
+  tl::ProfScope prof(tl::PROF_ADV, static_cast<cudaStream_t>(stream));
+  tl::RewardSpec rs{*params,    correct,     tool_called, n_vo,    r_acc,
+                    tests_pass, rewards_out, rapr_out,    rapr_in};
+  tl::group_adv_kernel<<<grid, tl::kAdvWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      rewards_out, group_off, n_groups, std_floor, nullptr, 0, 1.0, 1.0, adv64, adv32, nullptr,
+      nullptr, rs);
   TL_LAUNCH_CHECK();
   tl::count_launch();
   return TL_OK;
