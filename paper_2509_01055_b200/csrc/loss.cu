@@ -12,8 +12,10 @@
 //   report64_kernel       cli.loss aggregation (cli.py:317-345).
 // fp32 performance mode (tl_loss_f32), also the back half of the fused
 // LM-head step:
-//   loss32_token_kernel   token-parallel fp32 terms, scaled gradient
-//   traj_reduce_kernel    one CTA per trajectory, fixed-shape tree in fp64
+//   loss32_traj_kernel    one CTA per trajectory: fp32 terms + scaled
+//                         gradient, fixed-shape tree into per-trajectory sums
+//   traj_reduce_kernel    (LM-head step) per-trajectory tree over per-token
+//                         terms written by the fused log-prob epilogue
 //   group_reduce_kernel   one thread per group (fixed order)
 //   report_kernel         one CTA, fixed order
 // Every reduction has a fixed shape independent of scheduling, so results are
@@ -175,36 +177,6 @@ __global__ void ratio64_kernel(const double* __restrict__ a, const double* __res
     out[i] = cr_exp(clamp20(__dadd_rn(a[i], -b[i])));
 }
 
-// ------------------------------------------------------------- fp32 path --
-__global__ void __launch_bounds__(256)
-    loss32_token_kernel(const float* __restrict__ lnew, const float* __restrict__ lold,
-                        const float* __restrict__ lref, const uint8_t* __restrict__ mask,
-                        const int32_t* __restrict__ tot, const float* __restrict__ adv,
-                        const float* __restrict__ traj_w, long long n, tl_loss_config cfg,
-                        float* __restrict__ term, float* __restrict__ k3o,
-                        uint8_t* __restrict__ flags, float* __restrict__ grad) {
-  const float lo = static_cast<float>(1.0 - cfg.eps_low), hi = static_cast<float>(1.0 + cfg.eps_high);
-  const float beta = static_cast<float>(cfg.kl_beta);
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x) {
-    if (cfg.use_mask && !mask[t]) {
-      term[t] = 0.f;
-      k3o[t] = 0.f;
-      flags[t] = 0;
-      if (grad) grad[t] = 0.f;
-      continue;
-    }
-    const int b = tot[t];
-    const float rf = cfg.has_ref ? lref[t] : 0.f;
-    const TokTermF o = grpo_token_f32(lnew[t], lold[t], rf, cfg.has_ref != 0 && rf == rf, adv[b],
-                                      lo, hi, beta, cfg.objective);
-    term[t] = o.term;
-    k3o[t] = o.k3;
-    flags[t] = o.flags;
-    if (grad) grad[t] = o.dterm * traj_w[b];
-  }
-}
-
 }  // namespace
 
 // One CTA per trajectory: fixed-shape tree over the trajectory's packed
@@ -334,6 +306,82 @@ __global__ void __launch_bounds__(256)
   rep[11] = agg == 1 ? term : obj;
 }
 
+// Fused standalone K3 (fp32): one CTA per trajectory computes the per-token
+// terms and gradient and reduces them in a fixed-shape tree straight into
+// traj_out — 13 B/token in (+4 with a reference), 4 B/token out.
+__global__ void __launch_bounds__(256)
+    loss32_traj_kernel(const float* __restrict__ lnew, const float* __restrict__ lold,
+                       const float* __restrict__ lref, const uint8_t* __restrict__ mask,
+                       const int32_t* __restrict__ cu, const float* __restrict__ adv,
+                       const float* __restrict__ traj_w, tl_loss_config cfg,
+                       float* __restrict__ grad, double* __restrict__ traj_out) {
+  constexpr int kV = 5;
+  __shared__ double sh[kV][256 / 32];
+  const int b = blockIdx.x;
+  const int t0 = cu[b], t1 = cu[b + 1];
+  const float a = adv[b];
+  const float wt = traj_w ? traj_w[b] : 0.f;
+  const float lo = static_cast<float>(1.0 - cfg.eps_low), hi = static_cast<float>(1.0 + cfg.eps_high);
+  const float beta = static_cast<float>(cfg.kl_beta);
+  double v[kV] = {0, 0, 0, 0, 0};  // term, k3, n_act, clipped, clamps
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    if (cfg.use_mask && !mask[t]) {
+      if (grad) grad[t] = 0.f;
+      continue;
+    }
+    const float rf = cfg.has_ref ? lref[t] : 0.f;
+    const TokTermF o = grpo_token_f32(lnew[t], lold[t], rf, cfg.has_ref != 0 && rf == rf, a, lo,
+                                      hi, beta, cfg.objective);
+    if (grad) grad[t] = o.dterm * wt;
+    v[0] += o.term;
+    v[1] += o.k3;
+    v[2] += 1.0;
+    v[3] += (o.flags & kFlagClipped) ? 1.0 : 0.0;
+    v[4] += (o.flags & kFlagClamped) ? 1.0 : 0.0;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    double x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sh[i][w] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[kV];
+    for (int i = 0; i < kV; ++i) {
+      double x = 0;
+      for (int j = 0; j < (int)(blockDim.x / 32); ++j) x += sh[i][j];
+      r[i] = x;
+    }
+    double* o = traj_out + static_cast<long long>(b) * 8;
+    o[0] = r[0];
+    o[1] = r[2];
+    o[2] = r[3];
+    o[3] = r[4];
+    o[4] = r[1];
+    o[5] = t1 - t0;
+    o[6] = 0;
+    o[7] = 0;
+  }
+}
+
+int launch_group_report(const double* traj_out, const int32_t* group_off, int n_traj,
+                        int n_groups, int agg, double* group_out, double* report,
+                        cudaStream_t st) {
+  if (n_groups > 0) {
+    group_reduce_kernel<<<(n_groups + 127) / 128, 128, 0, st>>>(traj_out, group_off, n_groups,
+                                                                group_out);
+    TL_LAUNCH_CHECK();
+    count_launch();
+  }
+  report_kernel<<<1, 256, 0, st>>>(group_out, traj_out, n_groups, n_traj, agg, report);
+  TL_LAUNCH_CHECK();
+  count_launch();
+  return TL_OK;
+}
+
 int launch_reductions(const float* term, const float* k3o, const uint8_t* flags, const float* ent,
                       const uint8_t* mask, int use_mask, const int32_t* cu, const int32_t* group_off,
                       int n_traj, int n_groups, int agg, double* traj_out, double* group_out,
@@ -431,10 +479,8 @@ extern "C" int tl_token_ratio_f64(const double* logp_new, const double* logp_old
 }
 
 extern "C" size_t tl_loss_f32_workspace_bytes(int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
+  (void)n_tokens;
   tl::Workspace w{nullptr, 0};
-  w.take<float>(n_tokens);
-  w.take<float>(n_tokens);
-  w.take<uint8_t>(n_tokens);
   w.take<double>(static_cast<size_t>(n_traj) * 8);
   w.take<double>(static_cast<size_t>(n_groups) * TL_GROUP_OUT_LEN);
   return w.used + 256;
@@ -451,25 +497,19 @@ extern "C" int tl_loss_f32(const float* logp_new, const float* logp_old, const f
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(!cfg->use_mask || mask, TL_ERR_INVALID_ARG, "use_mask without mask");
   TL_REQUIRE(!grad || traj_w, TL_ERR_INVALID_ARG, "grad requires traj_w");
+  (void)traj_of_token;  // the fused kernel walks trajectories via cu_seqlens
   tl::Workspace w{static_cast<char*>(workspace), workspace_bytes};
-  float* term = w.take<float>(n_tokens);
-  float* k3o = w.take<float>(n_tokens);
-  uint8_t* flags = w.take<uint8_t>(n_tokens);
   double* traj_out = w.take<double>(static_cast<size_t>(n_traj) * 8);
   double* group_out = w.take<double>(static_cast<size_t>(n_groups) * TL_GROUP_OUT_LEN);
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "loss_f32 workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (n_tokens > 0) {
-    tl::ProfScope prof(tl::PROF_LOSS, st);
-    const long long blocks = (n_tokens + 255) / 256;
-    const int grid = static_cast<int>(blocks > 148 * 16 ? 148 * 16 : blocks);
-    tl::loss32_token_kernel<<<grid, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, traj_of_token,
-                                                  adv32, traj_w, n_tokens, *cfg, term, k3o, flags,
-                                                  grad);
+  tl::ProfScope prof(tl::PROF_LOSS, st);
+  if (n_traj > 0) {
+    tl::loss32_traj_kernel<<<n_traj, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, cu_seqlens,
+                                                   adv32, traj_w, *cfg, grad, traj_out);
     TL_LAUNCH_CHECK();
     tl::count_launch();
   }
-  return tl::launch_reductions(term, k3o, flags, nullptr, mask, cfg->use_mask, cu_seqlens,
-                               group_off, n_traj, n_groups, cfg->agg, traj_out, group_out, report,
-                               st);
+  return tl::launch_group_report(traj_out, group_off, n_traj, n_groups, cfg->agg, group_out, report,
+                                 st);
 }
