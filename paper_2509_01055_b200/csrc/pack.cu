@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(kScanThreads)
     pack_scan_kernel(const int32_t* __restrict__ seg_len, const uint8_t* __restrict__ seg_is_action,
                      const int32_t* __restrict__ traj_seg_off, int n_traj, int n_seg,
                      int32_t* __restrict__ seg_dst, int32_t* __restrict__ seg_act_dst,
-                     int32_t* __restrict__ seg_traj, int32_t* __restrict__ cu_seqlens,
-                     int32_t* __restrict__ act_off) {
+                     int32_t* __restrict__ seg_traj, int32_t* __restrict__ seg_tstart,
+                     int32_t* __restrict__ cu_seqlens, int32_t* __restrict__ act_off) {
   __shared__ ScanPair warp_tot[kScanThreads / 32];
   __shared__ ScanPair carry_sh;
   const int tid = threadIdx.x;
@@ -93,8 +93,12 @@ __global__ void __launch_bounds__(kScanThreads)
   const int total = carry.a, total_act = carry.b;
   for (int b = tid; b < n_traj; b += kScanThreads) {
     const int s0 = traj_seg_off[b], s1 = traj_seg_off[b + 1];
-    for (int s = s0; s < s1; ++s) seg_traj[s] = b;
-    cu_seqlens[b] = s0 < n_seg ? seg_dst[s0] : total;
+    const int start = s0 < n_seg ? seg_dst[s0] : total;
+    for (int s = s0; s < s1; ++s) {
+      seg_traj[s] = b;
+      seg_tstart[s] = start;
+    }
+    cu_seqlens[b] = start;
     act_off[b] = s0 < n_seg ? seg_act_dst[s0] : total_act;
   }
   if (tid == 0) {
@@ -116,46 +120,115 @@ __device__ __forceinline__ int find_segment(const int32_t* __restrict__ seg_dst,
   return lo - 1;
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kScatterThreads = 256;
+constexpr int kScatterRounds = 4;
+constexpr int kTilePos = kScatterThreads * 4 * kScatterRounds;  // packed positions per CTA
+constexpr int kSegCap = 1024;                                    // staged segments per CTA
+
+// Per-segment metadata, staged in shared memory for the segments a CTA's tile
+// overlaps (global fallback when a tile spans more than kSegCap segments).
+struct SegView {
+  const int32_t* dst;
+  const int32_t* len;
+  const int32_t* src;
+  const int32_t* act;
+  const int32_t* tstart;  // cu_seqlens of the segment's trajectory
+  const int32_t* traj;
+  const uint8_t* is_act;
+};
+
+template <bool kShared>
+__device__ __forceinline__ void scatter_rounds(const SegView v, int s_lo, int n_local,
+                                               long long tile_begin, long long tile_end,
+                                               const int32_t* __restrict__ pool, int32_t* ids,
+                                               uint8_t* mask, int32_t* pos, int32_t* tot,
+                                               int32_t* act_idx) {
+#pragma unroll 1
+  for (int r = 0; r < kScatterRounds; ++r) {
+    const long long p0 = tile_begin + (static_cast<long long>(r) * kScatterThreads + threadIdx.x) * 4;
+    if (p0 >= tile_end) return;
+    // segment of p0: last local segment with dst <= p0
+    int lo = 0, hi = n_local;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v.dst[mid] <= p0) lo = mid + 1;
+      else hi = mid;
+    }
+    int s = lo - 1;
+    int o_ids[4], o_pos[4], o_tot[4];
+    uint8_t o_m[4];
+    const int cnt = tile_end - p0 >= 4 ? 4 : static_cast<int>(tile_end - p0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= cnt) break;
+      const int p = static_cast<int>(p0) + j;
+      while (p >= v.dst[s] + v.len[s]) ++s;
+      const int off = p - v.dst[s];
+      const uint8_t a = v.is_act[s];
+      o_ids[j] = __ldg(pool + v.src[s] + off);
+      o_m[j] = a;
+      o_tot[j] = v.traj[s];
+      o_pos[j] = p - v.tstart[s];
+      if (a) act_idx[v.act[s] + off] = p;
+    }
+    if (cnt == 4) {
+      *reinterpret_cast<int4*>(ids + p0) = make_int4(o_ids[0], o_ids[1], o_ids[2], o_ids[3]);
+      *reinterpret_cast<int4*>(pos + p0) = make_int4(o_pos[0], o_pos[1], o_pos[2], o_pos[3]);
+      *reinterpret_cast<int4*>(tot + p0) = make_int4(o_tot[0], o_tot[1], o_tot[2], o_tot[3]);
+      *reinterpret_cast<uchar4*>(mask + p0) = make_uchar4(o_m[0], o_m[1], o_m[2], o_m[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // static indices keep o_*[] in registers
+        if (j < cnt) {
+          ids[p0 + j] = o_ids[j];
+          pos[p0 + j] = o_pos[j];
+          tot[p0 + j] = o_tot[j];
+          mask[p0 + j] = o_m[j];
+        }
+      }
+    }
+  }
+  (void)s_lo;
+}
+
+__global__ void __launch_bounds__(kScatterThreads)
     pack_scatter_kernel(const int32_t* __restrict__ pool, const int32_t* __restrict__ seg_src_off,
                         const int32_t* __restrict__ seg_len, const uint8_t* __restrict__ seg_is_action,
                         const int32_t* __restrict__ seg_dst, const int32_t* __restrict__ seg_act_dst,
-                        const int32_t* __restrict__ seg_traj, const int32_t* __restrict__ cu_seqlens,
+                        const int32_t* __restrict__ seg_traj, const int32_t* __restrict__ seg_tstart,
                         int n_seg, long long n_tokens, int32_t* __restrict__ ids,
                         uint8_t* __restrict__ mask, int32_t* __restrict__ pos,
                         int32_t* __restrict__ tot, int32_t* __restrict__ act_idx) {
-  const long long p0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  if (p0 >= n_tokens) return;
-  int s = find_segment(seg_dst, n_seg, static_cast<int>(p0));
-  int o_ids[4], o_pos[4], o_tot[4];
-  uint8_t o_m[4];
-  const int cnt = n_tokens - p0 >= 4 ? 4 : static_cast<int>(n_tokens - p0);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (j >= cnt) break;
-    const int p = static_cast<int>(p0) + j;
-    while (p >= __ldg(seg_dst + s) + __ldg(seg_len + s)) ++s;
-    const int off = p - __ldg(seg_dst + s);
-    const int b = __ldg(seg_traj + s);
-    const uint8_t is_act = __ldg(seg_is_action + s);
-    o_ids[j] = __ldg(pool + __ldg(seg_src_off + s) + off);
-    o_m[j] = is_act;
-    o_tot[j] = b;
-    o_pos[j] = p - __ldg(cu_seqlens + b);
-    if (is_act) act_idx[__ldg(seg_act_dst + s) + off] = p;
+  __shared__ int32_t sh_dst[kSegCap], sh_len[kSegCap], sh_src[kSegCap], sh_act[kSegCap],
+      sh_ts[kSegCap], sh_traj[kSegCap];
+  __shared__ uint8_t sh_isa[kSegCap];
+  __shared__ int sh_range[2];
+  const long long tile_begin = static_cast<long long>(blockIdx.x) * kTilePos;
+  const long long tile_end = min(n_tokens, tile_begin + kTilePos);
+  if (threadIdx.x == 0) {
+    sh_range[0] = find_segment(seg_dst, n_seg, static_cast<int>(tile_begin));
+    sh_range[1] = find_segment(seg_dst, n_seg, static_cast<int>(tile_end - 1));
   }
-  if (cnt == 4) {
-    *reinterpret_cast<int4*>(ids + p0) = make_int4(o_ids[0], o_ids[1], o_ids[2], o_ids[3]);
-    *reinterpret_cast<int4*>(pos + p0) = make_int4(o_pos[0], o_pos[1], o_pos[2], o_pos[3]);
-    *reinterpret_cast<int4*>(tot + p0) = make_int4(o_tot[0], o_tot[1], o_tot[2], o_tot[3]);
-    *reinterpret_cast<uchar4*>(mask + p0) = make_uchar4(o_m[0], o_m[1], o_m[2], o_m[3]);
-  } else {
-    for (int j = 0; j < cnt; ++j) {
-      ids[p0 + j] = o_ids[j];
-      pos[p0 + j] = o_pos[j];
-      tot[p0 + j] = o_tot[j];
-      mask[p0 + j] = o_m[j];
+  __syncthreads();
+  const int s_lo = sh_range[0], n_local = sh_range[1] - s_lo + 1;
+  if (n_local <= kSegCap) {
+    for (int i = threadIdx.x; i < n_local; i += kScatterThreads) {
+      const int s = s_lo + i;
+      sh_dst[i] = seg_dst[s];
+      sh_len[i] = seg_len[s];
+      sh_src[i] = seg_src_off[s];
+      sh_act[i] = seg_act_dst[s];
+      sh_ts[i] = seg_tstart[s];
+      sh_traj[i] = seg_traj[s];
+      sh_isa[i] = seg_is_action[s];
     }
+    __syncthreads();
+    const SegView v{sh_dst, sh_len, sh_src, sh_act, sh_ts, sh_traj, sh_isa};
+    scatter_rounds<true>(v, s_lo, n_local, tile_begin, tile_end, pool, ids, mask, pos, tot,
+                         act_idx);
+  } else {
+    const SegView v{seg_dst, seg_len, seg_src_off, seg_act_dst, seg_tstart, seg_traj, seg_is_action};
+    scatter_rounds<false>(v, 0, n_seg, tile_begin, tile_end, pool, ids, mask, pos, tot, act_idx);
   }
 }
 
@@ -180,9 +253,7 @@ __global__ void pack_padded_kernel(const int32_t* __restrict__ ids, const uint8_
 extern "C" size_t tl_pack_workspace_bytes(int32_t n_traj, int32_t n_seg) {
   (void)n_traj;
   tl::Workspace w{nullptr, 0};
-  w.take<int32_t>(n_seg);
-  w.take<int32_t>(n_seg);
-  w.take<int32_t>(n_seg);
+  for (int i = 0; i < 4; ++i) w.take<int32_t>(n_seg);
   return w.used + 256;
 }
 
@@ -199,22 +270,21 @@ extern "C" int tl_pack_varlen(const int32_t* token_pool, const int32_t* seg_src_
   int32_t* seg_dst = w.take<int32_t>(n_seg);
   int32_t* seg_act = w.take<int32_t>(n_seg);
   int32_t* seg_traj = w.take<int32_t>(n_seg);
+  int32_t* seg_tstart = w.take<int32_t>(n_seg);
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "pack workspace too small (%zu < %zu)", workspace_bytes,
              w.used);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   tl::ProfScope prof(tl::PROF_PACK, st);
   tl::pack_scan_kernel<<<1, tl::kScanThreads, 0, st>>>(seg_len, seg_is_action, traj_seg_off, n_traj,
-                                                       n_seg, seg_dst, seg_act, seg_traj, cu_seqlens,
-                                                       act_off);
+                                                       n_seg, seg_dst, seg_act, seg_traj,
+                                                       seg_tstart, cu_seqlens, act_off);
   TL_LAUNCH_CHECK();
   tl::count_launch();
   if (n_tokens > 0) {
-    const long long threads = (n_tokens + 3) / 4;
-    const int grid = static_cast<int>((threads + 255) / 256);
-    tl::pack_scatter_kernel<<<grid, 256, 0, st>>>(token_pool, seg_src_off, seg_len, seg_is_action,
-                                                  seg_dst, seg_act, seg_traj, cu_seqlens, n_seg,
-                                                  n_tokens, input_ids, loss_mask, position_ids,
-                                                  traj_of_token, act_idx);
+    const int grid = static_cast<int>((n_tokens + tl::kTilePos - 1) / tl::kTilePos);
+    tl::pack_scatter_kernel<<<grid, tl::kScatterThreads, 0, st>>>(
+        token_pool, seg_src_off, seg_len, seg_is_action, seg_dst, seg_act, seg_traj, seg_tstart,
+        n_seg, n_tokens, input_ids, loss_mask, position_ids, traj_of_token, act_idx);
     TL_LAUNCH_CHECK();
     tl::count_launch();
   }

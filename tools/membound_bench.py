@@ -21,7 +21,10 @@ PEAK = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").
 FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
-def timed(fn, iters=10):
+def timed(fn, iters=None):
+    import os
+
+    iters = int(os.environ.get("MEMBOUND_ITERS", "10")) if iters is None else iters
     ts = []
     for _ in range(iters + 2):
         FLUSH.fill_(1)
