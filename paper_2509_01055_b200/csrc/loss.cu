@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(256)
   const float lo = static_cast<float>(1.0 - cfg.eps_low), hi = static_cast<float>(1.0 + cfg.eps_high);
   const float beta = static_cast<float>(cfg.kl_beta);
   double v[kV] = {0, 0, 0, 0, 0};  // term, k3, n_act, clipped, clamps
+#pragma unroll 4
   for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     if (cfg.use_mask && !mask[t]) {
       if (grad) grad[t] = 0.f;
