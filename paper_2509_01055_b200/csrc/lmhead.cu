@@ -8,11 +8,14 @@
 //   fwd GEMM    z = h_c W^T tile by tile (128 x 256, K = H) in TMEM; the
 //               epilogue keeps, per row and per vocab strip, the online
 //               log-sum-exp state (max, sum e^(z-max), sum e^(z-max) z) and
-//               the target logit -> partials [n_strips, C]      (z never stored)
-//   combine     merge strips -> lse, logp = z_y - lse, entropy; the GRPO
-//               surrogate (grpo_token.cuh) runs right here on logp_new:
-//               per-token term / k3 / flags and dLoss/dlogp, dLoss/dent
-//   recompute   same GEMM, epilogue writes dS = dLoss/dz (bf16, [C, V])
+//               the target logit -> partials [n_strips, C]; the CTA that
+//               finishes the last strip of a 128-row block merges the strips
+//               (lse, logp = z_y - lse, entropy) and runs the GRPO surrogate
+//               (grpo_token.cuh) on logp_new in the same epilogue: per-token
+//               term / k3 / flags and dLoss/dlogp, dLoss/dent.  In store mode
+//               the epilogue also writes the chunk's logits as fp16.
+//   dsoftmax    (store mode) fp16 z -> bf16 dS in place, HBM-bound
+//   recompute   (recompute mode) same GEMM, epilogue writes dS (bf16, [C, V])
 //               dS = g (onehot(y) - p) - c p (z - E_p z),  p = e^(z - lse)
 //   dH GEMM     dhidden[act_idx] = dS W          (A K-major, B = W MN-major)
 //   dW GEMM     dW (+)= dS^T h_c                 (A, B MN-major; fp32 RMW)
@@ -164,6 +167,80 @@ __device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&
   }
 }
 
+struct CombineArgs {
+  const float4* part;
+  int n_strips, rows;
+  const int32_t* idx;  // row -> packed position (nullable: identity)
+  // forward-only outputs (indexed by row)
+  float* logp_row;
+  float* ent_row;
+  float* lse_row;
+  // fused loss (nullable block: forward-only when logp_old == nullptr)
+  const int32_t* traj_of_token;
+  const float* logp_old;
+  const float* logp_ref;
+  const float* adv;
+  const float* traj_w;
+  tl_loss_config cfg;
+  float ent_grad;        // dLoss/dentropy per action token
+  float* logp_out;       // [T]
+  float* ent_out;        // [T]
+  float* term;           // [T]
+  float* k3o;            // [T]
+  uint8_t* flags;        // [T]
+  float* g_row;          // [C]
+  float* c_row;          // [C]
+  float* ez_row;         // [C]
+};
+
+// Merge a row's vocab-strip partials -> lse, logp, entropy; then the GRPO
+// surrogate on logp_new (grpo_token.cuh) -> per-token term / k3 / flags and
+// the row's dLoss/dlogp, dLoss/dent (K3 math fused into the log-prob
+// epilogue).  Partials written by other CTAs are read with ld.global.cg.
+__device__ void combine_row(const CombineArgs& a, int r) {
+  float m = -INFINITY, s = 0.f, t = 0.f, zy = -INFINITY;
+  for (int j = 0; j < a.n_strips; ++j) {
+    const float4 q = __ldcg(a.part + static_cast<long long>(j) * a.rows + r);
+    zy = fmaxf(zy, q.w);
+    if (q.x == -INFINITY) continue;
+    if (q.x > m) {
+      const float f = expf(m - q.x);
+      s = s * f + q.y;
+      t = t * f + q.z;
+      m = q.x;
+    } else {
+      const float f = expf(q.x - m);
+      s += q.y * f;
+      t += q.z * f;
+    }
+  }
+  const float lse = m + logf(s);
+  const float ez = t / s;
+  const float logp = zy - lse;
+  const float ent = lse - ez;
+  if (a.logp_row) a.logp_row[r] = logp;
+  if (a.ent_row) a.ent_row[r] = ent;
+  if (a.lse_row) a.lse_row[r] = lse;
+  if (a.logp_old) {
+    const long long p = a.idx ? a.idx[r] : r;
+    const int b = a.traj_of_token[p];
+    const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
+    const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
+    const float rf = a.cfg.has_ref ? a.logp_ref[p] : 0.f;
+    const TokTermF o = grpo_token_f32(logp, a.logp_old[p], rf, a.cfg.has_ref != 0 && rf == rf,
+                                      a.adv[b], lo, hi, static_cast<float>(a.cfg.kl_beta),
+                                      a.cfg.objective);
+    a.logp_out[p] = logp;
+    a.ent_out[p] = ent;
+    a.term[p] = o.term;
+    a.k3o[p] = o.k3;
+    a.flags[p] = o.flags;
+    a.g_row[r] = -o.dterm * a.traj_w[b];  // loss = -objective
+    a.c_row[r] = a.ent_grad;
+    a.ez_row[r] = ez;
+  }
+}
+
 // Online log-sum-exp over a vocab strip; one thread = one token row.
 struct EpiLseStats {
   struct Params {
@@ -172,6 +249,8 @@ struct EpiLseStats {
     int rows;                // C (partials row stride)
     __half_raw* zout;        // optional fp16 logit tile store [C, ldz] (backward input)
     long long ldz;
+    int* tile_ctr;           // [ceil(C/128)] strips finished per 128-row block (zeroed)
+    CombineArgs ca;          // last-strip fixup: merge + surrogate for the block's rows
   };
   struct State {
     float m, s, t, zy;
@@ -225,10 +304,31 @@ struct EpiLseStats {
       st.t += t;
     }
   }
+  // Publish this strip's row stats; the CTA that finishes the LAST strip of a
+  // 128-row block (stream-K style fixup, counter per block) merges all strips
+  // and runs the GRPO surrogate for those rows inside this epilogue.
   __device__ static void end_unit(const Params& p, const GemmShape& sh, State& st, int row,
                                   const UnitCoord& uc) {
     if (row < sh.M)
       p.part[static_cast<long long>(uc.strip_idx) * p.rows + row] = make_float4(st.m, st.s, st.t, st.zy);
+    if (sh.n_strips == 1) {  // no other strip: merge straight away (own writes)
+      if (row < sh.M) combine_row(p.ca, row);
+      return;
+    }
+    __shared__ int s_last;
+    __threadfence();                                                   // release partials
+    asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");         // 4 epilogue warps
+    if ((threadIdx.x & 127) == 0) {
+      const int blk = row / kBM;
+      const int prev = atomicAdd(p.tile_ctr + blk, 1);
+      s_last = prev == sh.n_strips - 1;
+      if (s_last) p.tile_ctr[blk] = 0;  // re-arm for the next launch
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");
+    if (s_last) {
+      __threadfence();  // acquire the other strips' partials
+      if (row < sh.M) combine_row(p.ca, row);
+    }
   }
 };
 
@@ -321,77 +421,6 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t
     dst[i] = src[idx ? idx[i] : i];
 }
 
-struct CombineArgs {
-  const float4* part;
-  int n_strips, rows;
-  const int32_t* idx;  // row -> packed position (nullable: identity)
-  // forward-only outputs (indexed by row)
-  float* logp_row;
-  float* ent_row;
-  float* lse_row;
-  // fused loss (nullable block: forward-only when logp_old == nullptr)
-  const int32_t* traj_of_token;
-  const float* logp_old;
-  const float* logp_ref;
-  const float* adv;
-  const float* traj_w;
-  tl_loss_config cfg;
-  float ent_grad;        // dLoss/dentropy per action token
-  float* logp_out;       // [T]
-  float* ent_out;        // [T]
-  float* term;           // [T]
-  float* k3o;            // [T]
-  uint8_t* flags;        // [T]
-  float* g_row;          // [C]
-  float* c_row;          // [C]
-  float* ez_row;         // [C]
-};
-
-__global__ void combine_kernel(CombineArgs a) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.rows) return;
-  float m = -INFINITY, s = 0.f, t = 0.f, zy = -INFINITY;
-  for (int j = 0; j < a.n_strips; ++j) {
-    const float4 q = a.part[static_cast<long long>(j) * a.rows + r];
-    zy = fmaxf(zy, q.w);
-    if (q.x == -INFINITY) continue;
-    if (q.x > m) {
-      const float f = expf(m - q.x);
-      s = s * f + q.y;
-      t = t * f + q.z;
-      m = q.x;
-    } else {
-      const float f = expf(q.x - m);
-      s += q.y * f;
-      t += q.z * f;
-    }
-  }
-  const float lse = m + logf(s);
-  const float ez = t / s;
-  const float logp = zy - lse;
-  const float ent = lse - ez;
-  if (a.logp_row) a.logp_row[r] = logp;
-  if (a.ent_row) a.ent_row[r] = ent;
-  if (a.lse_row) a.lse_row[r] = lse;
-  if (a.logp_old) {
-    const long long p = a.idx ? a.idx[r] : r;
-    const int b = a.traj_of_token[p];
-    const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
-    const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
-    const float rf = a.cfg.has_ref ? a.logp_ref[p] : 0.f;
-    const TokTermF o = grpo_token_f32(logp, a.logp_old[p], rf, a.cfg.has_ref != 0 && rf == rf,
-                                      a.adv[b], lo, hi,
-                                      static_cast<float>(a.cfg.kl_beta), a.cfg.objective);
-    a.logp_out[p] = logp;
-    a.ent_out[p] = ent;
-    a.term[p] = o.term;
-    a.k3o[p] = o.k3;
-    a.flags[p] = o.flags;
-    a.g_row[r] = -o.dterm * a.traj_w[b];  // loss = -objective
-    a.c_row[r] = a.ent_grad;
-    a.ez_row[r] = ez;
-  }
-}
 
 // In place: fp16 logits z (written by the forward epilogue) -> bf16
 // dS = g (onehot(y) - p) - c p (z - E_p z), p = exp(z - lse).  One CTA per row.
@@ -510,7 +539,7 @@ ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool
   c.flags = w.take<uint8_t>(T);
   c.traj_out = w.take<double>(static_cast<size_t>(B) * 8);
   c.group_out = w.take<double>(static_cast<size_t>(G) * TL_GROUP_OUT_LEN);
-  c.sync = w.take<int>(4 * kSyncWaves);
+  c.sync = w.take<int>(5 * kSyncWaves);
   return c;
 }
 
@@ -535,19 +564,15 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
   CUtensorMap ma, mb;
   if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
   // fresh wave-lockstep counters for this chunk's GEMMs (fwd / dS / dH / dW)
-  TL_CUDA_TRY(cudaMemsetAsync(c.sync, 0, 4 * kSyncWaves * sizeof(int), st));
+  // and the per-128-row strip counters of the fused merge + surrogate
+  TL_CUDA_TRY(cudaMemsetAsync(c.sync, 0, 5 * kSyncWaves * sizeof(int), st));
+  TL_REQUIRE((rows + kBM - 1) / kBM <= kSyncWaves, TL_ERR_UNSUPPORTED, "chunk_rows too large");
   const GemmShape s = fwd_shape(rows, V, H, c.sync);
-  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz};
-  if (int e = launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD))
-    return e;
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
-  ProfScope prof(PROF_COMBINE, st);
-  combine_kernel<<<(rows + 127) / 128, 128, 0, st>>>(ca);
-  TL_LAUNCH_CHECK();
-  count_launch();
-  return TL_OK;
+  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, c.sync + 4 * kSyncWaves, ca};
+  return launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD);
 }
 
 }  // namespace
