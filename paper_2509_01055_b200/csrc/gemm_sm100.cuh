@@ -406,11 +406,17 @@ struct EpiStoreBF16 {
 };
 
 // fp32 store or accumulate (out += acc), used for dW across token chunks.
+// Accumulation is a fire-and-forget vector reduction at L2 (red.add.v4.f32)
+// unless `load_add` is set (load + add + store): the dW tile is BN = 512 wide
+// and single-buffered in TMEM, so an epilogue waiting on 512 loads per row
+// would stall the next tile's MMAs.  Each element has one writer per launch,
+// so both forms give the same bits.
 struct EpiStoreF32 {
   struct Params {
     float* out;
     long long ldo;
     int accumulate;
+    int load_add;
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -432,6 +438,10 @@ struct EpiStoreF32 {
         for (int j = 0; j < 32; j += 4) {
           float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                  __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          if (p.accumulate && !p.load_add) {
+            red_add_v4_f32(dst + j, v);
+            continue;
+          }
           if (p.accumulate) {
             const float4 o = *reinterpret_cast<const float4*>(dst + j);
             v.x += o.x;

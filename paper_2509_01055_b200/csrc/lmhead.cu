@@ -148,7 +148,11 @@ __device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
 }
 
 // 32 consecutive fp32 accumulator columns -> fp16 (saturating), 4 x 16-byte stores.
-__device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&r)[32], int nvalid) {
+// The stores carry an L2 eviction hint (`pol`): the chunk's logits are only
+// read back by the next kernel, so they should not push the wave's resident
+// h_c rows out of L2.
+__device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&r)[32], int nvalid,
+                                              uint64_t pol) {
   if (nvalid >= 32) {
 #pragma unroll
     for (int j = 0; j < 32; j += 8) {
@@ -157,7 +161,7 @@ __device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&
       v.y = pack_f16x2_sat(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
       v.z = pack_f16x2_sat(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
       v.w = pack_f16x2_sat(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
-      *reinterpret_cast<uint4*>(dst + j) = v;
+      st_v4_hint(dst + j, v, pol);
     }
   } else {
 #pragma unroll
@@ -251,10 +255,12 @@ struct EpiLseStats {
     long long ldz;
     int* tile_ctr;           // [ceil(C/128)] strips finished per 128-row block (zeroed)
     CombineArgs ca;          // last-strip fixup: merge + surrogate for the block's rows
+    int z_policy;            // make_policy() kind of the fp16 logit stores
   };
   struct State {
     float m, s, t, zy;
     int y;
+    uint64_t zpol;
   };
   __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
                                     const UnitCoord&) {
@@ -263,6 +269,7 @@ struct EpiLseStats {
     st.t = 0.f;
     st.zy = -INFINITY;
     st.y = row < sh.M ? p.targets[row] : -1;
+    st.zpol = make_policy(p.z_policy);
   }
   template <int BN>
   __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
@@ -274,7 +281,7 @@ struct EpiLseStats {
       tmem_ld_wait();
       const int cb = col0 + c;
       const int nvalid = sh.N - cb;  // columns >= N are padding
-      if (p.zout && row < sh.M) store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid);
+      if (p.zout && row < sh.M) store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid, st.zpol);
       float cm = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -499,6 +506,12 @@ struct ChunkWs {
 
 constexpr int kSyncWaves = 4096;
 
+// Tuning overrides (profiling only).
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // Tuning overrides (profiling only): TL_SYNC_<name>=every,window ; every=0 disables.
 void sync_override(const char* name, int& every, int& window) {
   char key[64];
@@ -571,7 +584,8 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
-  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, c.sync + 4 * kSyncWaves, ca};
+  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, c.sync + 4 * kSyncWaves, ca,
+                         env_int("TL_Z_POLICY", 1)};
   return launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD);
 }
 
@@ -602,7 +616,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
   if (c_fp32 && N >= 1024) {  // wide 256 x 512 pair tiles (as the dH / dW GEMMs)
     const GemmShape s = make_shape(M, N, K, kBNWide, 1, kGroupM, kCG);
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
@@ -612,7 +626,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   }
   const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   if (c_fp32) {
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32>(ma, mb, s, ep, st);
@@ -784,7 +798,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
         return e;
       const GemmShape s = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
                                     c.sync + 3 * kSyncWaves, 8, 2, "DW");
-      EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0};
+      EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
       if (int e = launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st,
                                                                      PROF_GEMM_DW))
         return e;

@@ -95,6 +95,22 @@ __device__ __forceinline__ uint64_t make_policy(int kind) {
   return kind == 2 ? policy_evict_last() : (kind == 1 ? policy_evict_first() : policy_evict_normal());
 }
 
+// ------------------------------------------------ epilogue global stores ----
+// Fire-and-forget fp32 vector add into global memory, performed at L2
+// (red.global.add.v4.f32, sm_90+): an accumulate epilogue never waits on a
+// load.  With a single writer per element the result equals load+add+store.
+__device__ __forceinline__ void red_add_v4_f32(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+// 16-byte store with an L2 eviction-priority hint (createpolicy).
+__device__ __forceinline__ void st_v4_hint(void* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
 // --------------------------------------------------- gpu-scope counters ----
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
