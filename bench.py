@@ -231,6 +231,9 @@ def main():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--chunk-rows", type=int, default=None)
+    ap.add_argument("--mode", default="store", choices=["store", "pipelined", "recompute"],
+                    help="LM-head backward schedule (TL_LMHEAD_* in include/toolloop_b200.h); "
+                         "store is fastest on a power-capped B200 (DESIGN.md §3)")
     args = ap.parse_args()
 
     from paper_2509_01055_b200.synthetic import CONFIGS
@@ -288,7 +291,8 @@ def main():
     wl.logp_old = lold.cpu().numpy()
     wl.logp_ref = lref.cpu().numpy()
     del packed0, lp_now, act_rows
-    step = grpo.GRPOStep(H, V, loss_cfg, chunk_rows=args.chunk_rows)
+    step = grpo.GRPOStep(H, V, loss_cfg, chunk_rows=args.chunk_rows,
+                         recompute=args.mode == "recompute", pipelined=args.mode == "pipelined")
     outputs = {
         "logp": torch.empty(T, dtype=torch.float32, device=dev),
         "entropy": torch.empty(T, dtype=torch.float32, device=dev),
@@ -425,7 +429,8 @@ def main():
                    "tokens_per_step": int(T_all), "action_tokens_per_step": int(A_all),
                    "action_tokens_per_s": A_all / (ms / 1e3),
                    "parallelism": f"dp{world} (groups, LPT)", "l2": "inputs >> L2 (hidden is GBs)",
-                   "chunk_rows": step._chunk(wl.n_act), "loss_agg": cfg.loss_agg},
+                   "chunk_rows": step._chunk(wl.n_act), "loss_agg": cfg.loss_agg,
+                   "lmhead_mode": args.mode},
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": int(launches),

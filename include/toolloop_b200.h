@@ -216,6 +216,14 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
  *    epilogue writes dS (8*T*H*V issued FLOPs; no logits ever leave TMEM). */
 #define TL_LMHEAD_STORE_LOGITS 0
 #define TL_LMHEAD_RECOMPUTE 1
+/*  STORE_LOGITS_PIPELINED: STORE_LOGITS with two chunk buffers; chunk i's
+ *    elementwise dS pass runs on an internal side stream concurrently with
+ *    chunk i+1's forward GEMM (workspace: tl_lmhead_step_workspace_bytes). */
+#define TL_LMHEAD_STORE_LOGITS_PIPELINED 2
+/* Workspace for tl_grpo_lmhead_step in `mode` (PIPELINED holds two chunks). */
+size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
+                                      int64_t n_tokens, int32_t n_traj, int32_t n_groups,
+                                      int32_t mode);
 /* Whole GRPO step on device-resident tensors:
  *   logp_new = LMhead(hidden[act rows]); surrogate (K3 math) fused into the
  *   log-prob epilogue; report; loss = -(objective + entropy_coef * mean

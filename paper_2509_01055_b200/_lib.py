@@ -34,7 +34,8 @@ EXPORTS = [
     "tl_group_advantages", "tl_group_rewards_advantages",
     "tl_loss_f64_workspace_bytes", "tl_loss_f64", "tl_report_f64", "tl_token_ratio_f64",
     "tl_loss_f32_workspace_bytes", "tl_loss_f32",
-    "tl_lmhead_workspace_bytes", "tl_lmhead_logprobs", "tl_grpo_lmhead_step",
+    "tl_lmhead_workspace_bytes", "tl_lmhead_step_workspace_bytes", "tl_lmhead_logprobs",
+    "tl_grpo_lmhead_step",
     "tl_gemm_bf16",
     "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
 ]
@@ -83,6 +84,7 @@ _SIGS = {
     "tl_loss_f32": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I64,
                               C.POINTER(LossConfigC), _P, _P, _P, _SZ, _P]),
     "tl_lmhead_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I64, _I32, _I32]),
+    "tl_lmhead_step_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I64, _I32, _I32, _I32]),
     "tl_lmhead_logprobs": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _I32, _P, _SZ,
                                      _P]),
     "tl_grpo_lmhead_step": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64,
@@ -164,6 +166,7 @@ def launch_count() -> int:
 N_PROF = 12
 LMHEAD_STORE_LOGITS = 0
 LMHEAD_RECOMPUTE = 1
+LMHEAD_STORE_LOGITS_PIPELINED = 2
 
 
 def profile_enable(on: bool = True) -> None:

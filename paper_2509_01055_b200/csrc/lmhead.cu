@@ -40,6 +40,7 @@ constexpr int kCG = 2;  // 2-CTA (cta_group::2) tiles of 256 x 256
 constexpr int kBNWide = 512;
 constexpr int kStages = 6;
 constexpr int kStripsFwd = 6;  // even: a wave covers 2 strips of one M group
+constexpr int kMaxStripsFwd = 64;  // partials capacity (profiling overrides)
 constexpr int kGroupM = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -431,12 +432,15 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t
 
 // In place: fp16 logits z (written by the forward epilogue) -> bf16
 // dS = g (onehot(y) - p) - c p (z - E_p z), p = exp(z - lse).  One CTA per row.
+// Rows are grid-strided: one CTA per row when launched alone, or a small
+// persistent grid when it runs beside the next chunk's forward GEMM
+// (pipelined mode) and should trickle at low HBM intensity.
 __global__ void __launch_bounds__(256)
-    dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec, int V,
+    dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec, int V, int rows,
                             const int32_t* __restrict__ y, const float* __restrict__ lse,
                             const float* __restrict__ g, const float* __restrict__ c,
                             const float* __restrict__ ez) {
-  const int r = blockIdx.x;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
   const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r], e = ez[r];
   const int yy = y[r];
   uint4* row = buf + static_cast<long long>(r) * ld_vec;
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(256)
       o[k] = pack_bf16x2(d0, d1);
     }
     row[v] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
   }
 }
 
@@ -486,7 +491,7 @@ int grid_for(long long n, int block) {
 // --------------------------------------------------------------- workspace --
 struct ChunkWs {
   uint16_t* h;      // [C, H]
-  float4* part;     // [kStripsFwd, C]
+  float4* part;     // [kMaxStripsFwd, C]
   int32_t* y;       // [C]
   float* lse;       // [C]
   float* g;         // [C]
@@ -535,10 +540,11 @@ GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* na
 
 long long vld_of(int vocab) { return (vocab + 7) / 8 * 8; }
 
-ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool with_bwd) {
-  ChunkWs c{};
+// Chunk buffers (h_c, partials, per-row stats, dS, lockstep counters) once,
+// or twice when `second` is given (pipelined mode); step-level buffers once.
+void carve_chunk(Workspace& w, ChunkWs& c, int C, int H, int V, bool with_bwd) {
   c.h = w.take<uint16_t>(static_cast<size_t>(C) * H);
-  c.part = w.take<float4>(static_cast<size_t>(kStripsFwd) * C);
+  c.part = w.take<float4>(static_cast<size_t>(kMaxStripsFwd) * C);
   c.y = w.take<int32_t>(C);
   c.lse = w.take<float>(C);
   c.g = w.take<float>(C);
@@ -547,26 +553,67 @@ ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool
   c.logp = w.take<float>(C);
   c.ent = w.take<float>(C);
   c.ds = with_bwd ? w.take<uint16_t>(static_cast<size_t>(C) * vld_of(V)) : nullptr;
+  c.sync = w.take<int>(5 * kSyncWaves);
+}
+
+ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool with_bwd,
+              ChunkWs* second = nullptr) {
+  ChunkWs c{};
+  carve_chunk(w, c, C, H, V, with_bwd);
+  if (second) carve_chunk(w, *second, C, H, V, with_bwd);
   c.term = w.take<float>(T);
   c.k3o = w.take<float>(T);
   c.flags = w.take<uint8_t>(T);
   c.traj_out = w.take<double>(static_cast<size_t>(B) * 8);
   c.group_out = w.take<double>(static_cast<size_t>(G) * TL_GROUP_OUT_LEN);
-  c.sync = w.take<int>(5 * kSyncWaves);
+  if (second) {
+    second->term = c.term;
+    second->k3o = c.k3o;
+    second->flags = c.flags;
+    second->traj_out = c.traj_out;
+    second->group_out = c.group_out;
+  }
   return c;
 }
+
+// A side stream + two events for one pipelined step (created per call so
+// concurrent callers never share them; destroyed asynchronously).
+struct StreamPair {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_ds = nullptr;
+  int err = TL_OK;
+  explicit StreamPair(cudaStream_t) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_ds, cudaEventDisableTiming) != cudaSuccess)
+      err = TL_ERR_CUDA;
+  }
+  ~StreamPair() {
+    if (ev_fwd) cudaEventDestroy(ev_fwd);
+    if (ev_ds) cudaEventDestroy(ev_ds);
+    if (side) cudaStreamDestroy(side);
+  }
+};
 
 // Forward LM-head GEMM shape: A-stationary strips.  A wave of n_pairs units
 // is 2 strips x (n_pairs / 2) M-tiles, so the wave's h_c rows (37 x 256 x H
 // bf16 = 67 MB at C2) stay in L2 (evict_last) across the strip while every
 // W tile is fetched once per wave and shared by the n_pairs / 2 pairs of its
-// strip, kept within 2 tiles of each other by the wave lockstep.
+// strip, kept within one tile of each other by the wave lockstep (window 1:
+// a producer may not start tile t before every CTA of the wave has issued
+// tile t-1).  Measured at C2 (tools/fwd_probe.py, ncu): window 2 -> 1 cuts
+// the forward's DRAM reads 33 -> 14 GB per chunk and the launch 3.5 %.
 GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int n_tiles = (V + kBN - 1) / kBN;
-  const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
-  const int group_m = num_sms() / kCG / 2;
-  GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, /*pol_a=*/2, /*pol_b=*/0);
-  return with_sync(s, sync, s.k_blocks, 2, "FWD");
+  int strips = env_int("TL_FWD_STRIPS", kStripsFwd);
+  strips = strips < 1 ? 1 : (strips > kMaxStripsFwd ? kMaxStripsFwd : strips);
+  const int strip = (n_tiles + strips - 1) / strips;
+  const int group_m = env_int("TL_FWD_GROUPM", num_sms() / kCG / 2);
+  GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, env_int("TL_FWD_POLA", 2),
+                           env_int("TL_FWD_POLB", 0));
+  return with_sync(s, sync, s.k_blocks, 1, "FWD");
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
@@ -598,6 +645,16 @@ extern "C" size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, 
                                             int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
   Workspace w{nullptr, 0};
   carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true);
+  return w.used + 1024;
+}
+
+extern "C" size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden,
+                                                 int32_t vocab, int64_t n_tokens, int32_t n_traj,
+                                                 int32_t n_groups, int32_t mode) {
+  Workspace w{nullptr, 0};
+  ChunkWs second{};
+  carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true,
+        mode == TL_LMHEAD_STORE_LOGITS_PIPELINED ? &second : nullptr);
   return w.used + 1024;
 }
 
@@ -686,8 +743,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                    double* report, int32_t chunk_rows, int32_t mode,
                                    void* workspace, size_t workspace_bytes, tl_stream_t stream) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
-  TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE, TL_ERR_INVALID_ARG,
-             "unknown lmhead mode %d", mode);
+  TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE ||
+                 mode == TL_LMHEAD_STORE_LOGITS_PIPELINED,
+             TL_ERR_INVALID_ARG, "unknown lmhead mode %d", mode);
   TL_REQUIRE(cfg->use_mask == 1, TL_ERR_UNSUPPORTED, "LM-head step computes action rows only");
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(H > 0 && V > 0 && chunk_rows > 0 && n_act >= 0, TL_ERR_INVALID_ARG, "bad sizes");
@@ -697,7 +755,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool bwd = dhidden != nullptr;
   Workspace w{static_cast<char*>(workspace), workspace_bytes};
-  ChunkWs c = carve(w, chunk_rows, H, V, n_tokens, n_traj, n_groups, bwd);
+  ChunkWs c2{};
+  ChunkWs c = carve(w, chunk_rows, H, V, n_tokens, n_traj, n_groups, bwd,
+                    mode == TL_LMHEAD_STORE_LOGITS_PIPELINED && bwd ? &c2 : nullptr);
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "lmhead workspace too small (%zu < %zu)", workspace_bytes,
              w.used);
   const long long Vld = vld_of(V);
@@ -722,19 +782,29 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     cudaMemsetAsync(dweight, 0, static_cast<size_t>(V) * H * sizeof(float), st);
   }
 
-  for (long long c0 = 0; c0 < n_act; c0 += chunk_rows) {
-    const int rows = static_cast<int>(n_act - c0 < chunk_rows ? n_act - c0 : chunk_rows);
-    const int32_t* ci = act_idx + c0;
+  const bool store = bwd && mode != TL_LMHEAD_RECOMPUTE;
+  const bool pipelined = bwd && mode == TL_LMHEAD_STORE_LOGITS_PIPELINED;
+  const long long n_chunks = (n_act + chunk_rows - 1) / chunk_rows;
+  auto rows_of = [&](long long i) {
+    const long long c0 = i * chunk_rows;
+    return static_cast<int>(n_act - c0 < chunk_rows ? n_act - c0 : chunk_rows);
+  };
+  const ChunkWs* bufs[2] = {&c, pipelined ? &c2 : &c};
+
+  // stage F: gather the chunk's action rows, fused forward (+ surrogate, + fp16 logits)
+  auto stage_fwd = [&](long long i) -> int {
+    const ChunkWs& b = *bufs[i & 1];
+    const int rows = rows_of(i);
+    const int32_t* ci = act_idx + i * chunk_rows;
     {
       ProfScope prof(PROF_GATHER, st);
       gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
-          reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(c.h));
+          reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(b.h));
       TL_LAUNCH_CHECK();
-      gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(input_ids, ci, rows, c.y);
+      gather_i32_kernel<<<grid_for(rows, 256), 256, 0, st>>>(input_ids, ci, rows, b.y);
       TL_LAUNCH_CHECK();
       count_launch(2);
     }
-
     CombineArgs ca{};
     ca.idx = ci;
     ca.traj_of_token = traj_of_token;
@@ -746,62 +816,87 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     ca.ent_grad = ent_grad;
     ca.logp_out = logp_out;
     ca.ent_out = entropy_out;
-    ca.term = c.term;
-    ca.k3o = c.k3o;
-    ca.flags = c.flags;
-    ca.g_row = c.g;
-    ca.c_row = c.c;
-    ca.ez_row = c.ez;
-    ca.lse_row = c.lse;
-    const bool store = bwd && mode == TL_LMHEAD_STORE_LOGITS;
-    if (int e = lmhead_forward_chunk(c, weight, rows, H, V, ca, st,
-                                     store ? reinterpret_cast<__half_raw*>(c.ds) : nullptr, Vld))
-      return e;
-    if (!bwd) continue;
-
+    ca.term = b.term;
+    ca.k3o = b.k3o;
+    ca.flags = b.flags;
+    ca.g_row = b.g;
+    ca.c_row = b.c;
+    ca.ez_row = b.ez;
+    ca.lse_row = b.lse;
+    return lmhead_forward_chunk(b, weight, rows, H, V, ca, st,
+                                store ? reinterpret_cast<__half_raw*>(b.ds) : nullptr, Vld);
+  };
+  // stage S: dS for the chunk (in place over its fp16 logits, or recomputed)
+  auto stage_ds = [&](long long i, cudaStream_t s_ds, int grid) -> int {
+    const ChunkWs& b = *bufs[i & 1];
+    const int rows = rows_of(i);
     if (store) {
-      // fp16 chunk logits -> bf16 dS in place (elementwise, HBM-bound)
-      ProfScope prof(PROF_DSOFTMAX, st);
-      dsoftmax_inplace_kernel<<<rows, 256, 0, st>>>(reinterpret_cast<uint4*>(c.ds), Vld / 8, V, c.y,
-                                                    c.lse, c.g, c.c, c.ez);
+      ProfScope prof(PROF_DSOFTMAX, s_ds);
+      dsoftmax_inplace_kernel<<<grid < rows ? grid : rows, 256, 0, s_ds>>>(
+          reinterpret_cast<uint4*>(b.ds), Vld / 8, V, rows, b.y, b.lse, b.g, b.c, b.ez);
       TL_LAUNCH_CHECK();
       count_launch();
-    } else {
-      // recompute z -> dS (bf16) in the GEMM epilogue
-      CUtensorMap ma, mb;
-      if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG))
-        return e;
-      const GemmShape s = fwd_shape(rows, V, H, c.sync + kSyncWaves);
-      EpiDSoftmax::Params ep{c.y, c.lse, c.g, c.c, c.ez,
-                             reinterpret_cast<__nv_bfloat16_raw*>(c.ds), Vld};
-      if (int e = launch_gemm<kCG, false, false, EpiDSoftmax>(ma, mb, s, ep, st, PROF_GEMM_DS))
-        return e;
+      return TL_OK;
     }
-    // dH rows = dS W  -> scattered to packed positions
+    CUtensorMap ma, mb;
+    if (int e = make_ab_maps(&ma, &mb, b.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
+    const GemmShape sh = fwd_shape(rows, V, H, b.sync + kSyncWaves);
+    EpiDSoftmax::Params ep{b.y, b.lse, b.g, b.c, b.ez,
+                           reinterpret_cast<__nv_bfloat16_raw*>(b.ds), Vld};
+    return launch_gemm<kCG, false, false, EpiDSoftmax>(ma, mb, sh, ep, s_ds, PROF_GEMM_DS);
+  };
+  // stage B: dH rows = dS W (scattered to packed positions), dW (+)= dS^T h_c
+  auto stage_bwd = [&](long long i) -> int {
+    const ChunkWs& b = *bufs[i & 1];
+    const int rows = rows_of(i);
+    const int32_t* ci = act_idx + i * chunk_rows;
     {
       CUtensorMap ma, mb;
-      if (int e = make_ab_maps(&ma, &mb, c.ds, false, rows, Vld, weight, true, H, H, V, kCG))
+      if (int e = make_ab_maps(&ma, &mb, b.ds, false, rows, Vld, weight, true, H, H, V, kCG))
         return e;
       // N-complete raster (group_m = 1): all H tiles of an M tile run together
       // so each dS k-block is fetched from HBM once; dS streams (evict first).
-      const GemmShape s = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
-                                    c.sync + 2 * kSyncWaves, 8, 2, "DH");
+      const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
+                                     b.sync + 2 * kSyncWaves, 8, 2, "DH");
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
-      if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, s, ep, st,
+      if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
         return e;
     }
-    // dW (+)= dS^T h_c
-    {
-      CUtensorMap ma, mb;
-      if (int e = make_ab_maps(&ma, &mb, c.ds, true, V, Vld, c.h, true, H, H, rows, kCG))
-        return e;
-      const GemmShape s = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
-                                    c.sync + 3 * kSyncWaves, 8, 2, "DW");
-      EpiStoreF32::Params ep{dweight, H, c0 > 0 ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
-      if (int e = launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st,
-                                                                     PROF_GEMM_DW))
-        return e;
+    CUtensorMap ma, mb;
+    if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
+    const GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
+                                   b.sync + 3 * kSyncWaves, 8, 2, "DW");
+    EpiStoreF32::Params ep{dweight, H, i > 0 ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
+    return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
+  };
+
+  if (!pipelined) {
+    for (long long i = 0; i < n_chunks; ++i) {
+      if (int e = stage_fwd(i)) return e;
+      if (!bwd) continue;
+      if (int e = stage_ds(i, st, 1 << 30)) return e;
+      if (int e = stage_bwd(i)) return e;
+    }
+  } else if (n_chunks > 0) {
+    // Two chunk buffers; chunk i's dS pass runs on a side stream beside chunk
+    // i+1's forward GEMM (the GEMM is tensor-bound and leaves HBM idle):
+    //   main: F0 F1 . B0 F2 . B1 F3 . B2 ...      side: S0 (|| F1)  S1 (|| F2) ...
+    // S_i is submitted after F_{i+1} so the GEMM's persistent CTAs are placed
+    // first and the pass (a small grid-strided grid) fills the remaining slots.
+    StreamPair sp(st);
+    if (sp.err) return sp.err;
+    const int ds_grid = env_int("TL_DS_OVERLAP_CTAS", 2) * num_sms();
+    if (int e = stage_fwd(0)) return e;
+    for (long long i = 0; i < n_chunks; ++i) {
+      TL_CUDA_TRY(cudaEventRecord(sp.ev_fwd, st));  // F_i done
+      if (i + 1 < n_chunks)
+        if (int e = stage_fwd(i + 1)) return e;     // buffer (i+1)&1, freed by B_{i-1}
+      TL_CUDA_TRY(cudaStreamWaitEvent(sp.side, sp.ev_fwd, 0));
+      if (int e = stage_ds(i, sp.side, ds_grid)) return e;
+      TL_CUDA_TRY(cudaEventRecord(sp.ev_ds, sp.side));
+      TL_CUDA_TRY(cudaStreamWaitEvent(st, sp.ev_ds, 0));
+      if (int e = stage_bwd(i)) return e;
     }
   }
   return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,

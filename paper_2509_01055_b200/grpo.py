@@ -108,21 +108,32 @@ class GRPOStep:
     backward, all on the device.  Reusable across steps (workspace cached)."""
 
     def __init__(self, hidden_dim: int, vocab: int, cfg: LossConfig | None = None,
-                 chunk_rows: int | None = None, recompute: bool = False):
+                 chunk_rows: int | None = None, recompute: bool = False,
+                 pipelined: bool = False):
         """recompute=False keeps each chunk's logits in fp16 for the backward
         (6*T*H*V FLOPs); True recomputes them in a second GEMM (8*T*H*V) so no
-        logit ever leaves TMEM (include/toolloop_b200.h, TL_LMHEAD_*)."""
+        logit ever leaves TMEM.  pipelined=True (store mode) double-buffers the
+        chunk workspace and runs each chunk's dS pass beside the next chunk's
+        forward GEMM (include/toolloop_b200.h, TL_LMHEAD_*); bitwise equal to
+        the serial schedule but measured 3 % slower at C2 on a power-capped
+        B200 (the GEMM slows by as much as the pass it hides), so off by
+        default."""
         self.H = int(hidden_dim)
         self.V = int(vocab)
         self.cfg = cfg or LossConfig()
         self.chunk_rows = chunk_rows
-        self.mode = _lib.LMHEAD_RECOMPUTE if recompute else _lib.LMHEAD_STORE_LOGITS
+        if recompute:
+            self.mode = _lib.LMHEAD_RECOMPUTE
+        elif pipelined:
+            self.mode = _lib.LMHEAD_STORE_LOGITS_PIPELINED
+        else:
+            self.mode = _lib.LMHEAD_STORE_LOGITS
         self._ws = _Workspace()
 
     def workspace_bytes(self, n_act: int, n_tokens: int, n_traj: int, n_groups: int) -> int:
         L = _lib.lib()
-        return int(L.tl_lmhead_workspace_bytes(self._chunk(n_act), self.H, self.V, n_tokens,
-                                               n_traj, n_groups))
+        return int(L.tl_lmhead_step_workspace_bytes(self._chunk(n_act), self.H, self.V, n_tokens,
+                                                    n_traj, n_groups, self.mode))
 
     def _chunk(self, n_act: int) -> int:
         if self.chunk_rows:
@@ -178,8 +189,8 @@ class GRPOStep:
         if rep is None:
             rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
         chunk = self._chunk(packed.n_act)
-        ws_bytes = int(L.tl_lmhead_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
-                                                   n_groups))
+        ws_bytes = int(L.tl_lmhead_step_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
+                                                        n_groups, self.mode))
         ws = self._ws.get(ws_bytes, dev)
         c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
         _lib.check(L.tl_grpo_lmhead_step(

@@ -1,6 +1,8 @@
 """Run-to-run determinism of the fused step (race detection /
 deterministic reductions): two identical GRPO steps must agree bitwise in
-every output — no float atomics anywhere on the path."""
+every output — no order-dependent float atomics anywhere on the path (the
+dW accumulation across chunks is a red.add with one writer per element per
+launch, so it is ordered by the stream)."""
 
 import numpy as np
 import pytest
@@ -15,8 +17,45 @@ from paper_2509_01055_b200.rl.loss import LossConfig  # noqa: E402
 from paper_2509_01055_b200.synthetic import CONFIGS, make_workload  # noqa: E402
 
 
-@pytest.mark.parametrize("recompute", [False, True])
-def test_step_bitwise_deterministic(recompute):
+MODES = {"store": {}, "recompute": {"recompute": True}, "pipelined": {"pipelined": True}}
+
+
+def _tiny_step_inputs():
+    cfg = CONFIGS["tiny"]
+    wl = make_workload(cfg)
+    H, V = cfg.hidden, cfg.vocab
+    packed = packing.pack_table(wl.table)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    h = torch.randn((wl.n_tokens, H), device="cuda", generator=g).bfloat16()
+    W = (torch.randn((V, H), device="cuda", generator=g) * 0.05).bfloat16()
+    lold = torch.from_numpy(wl.logp_old).cuda()
+    lref = torch.from_numpy(wl.logp_ref).cuda()
+    return wl, H, V, packed, h, W, lold, lref
+
+
+def _outputs(r):
+    return (r.report_tensor.clone(), r.logp.clone(), r.entropy.clone(), r.dhidden.clone(),
+            r.dweight.clone())
+
+
+@pytest.mark.parametrize("chunk", [128, 256])
+def test_pipelined_equals_serial_bitwise(chunk):
+    """The pipelined schedule (dS pass on a side stream beside the next
+    chunk's forward, two chunk buffers) runs the same kernels on the same
+    data: every output equals the serial store-logits schedule bitwise."""
+    wl, H, V, packed, h, W, lold, lref = _tiny_step_inputs()
+    cfg = LossConfig(kl_beta=0.04, entropy_coef=0.01)
+    a = _outputs(grpo.GRPOStep(H, V, cfg, chunk_rows=chunk)(
+        packed, wl.group_off, wl.rewards, h, W, lold, lref))
+    b = _outputs(grpo.GRPOStep(H, V, cfg, chunk_rows=chunk, pipelined=True)(
+        packed, wl.group_off, wl.rewards, h, W, lold, lref))
+    assert packed.n_act > 2 * chunk  # several chunks, both buffers in use
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_step_bitwise_deterministic(mode):
     cfg = CONFIGS["tiny"]
     wl = make_workload(cfg)
     H, V = cfg.hidden, cfg.vocab
@@ -27,7 +66,7 @@ def test_step_bitwise_deterministic(recompute):
     lold = torch.from_numpy(wl.logp_old).cuda()
     lref = torch.from_numpy(wl.logp_ref).cuda()
     step = grpo.GRPOStep(H, V, LossConfig(kl_beta=0.04, entropy_coef=0.01), chunk_rows=256,
-                         recompute=recompute)
+                         **MODES[mode])
     outs = []
     for _ in range(2):
         r = step(packed, wl.group_off, wl.rewards, h, W, lold, lref)

@@ -360,9 +360,12 @@ def _rel_fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("recompute", [False, True])
+MODES = {"store": {}, "recompute": {"recompute": True}, "pipelined": {"pipelined": True}}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256), (192, 517, 128)])
-def test_grpo_lmhead_step_vs_oracle(H, V, chunk, recompute):
+def test_grpo_lmhead_step_vs_oracle(H, V, chunk, mode):
     from oracle import lmhead_oracle as LH
 
     trajs, rewards, go, _, lold, lref = _synthetic_batch(4, n_groups=6, G=4)
@@ -376,7 +379,7 @@ def test_grpo_lmhead_step_vs_oracle(H, V, chunk, recompute):
     W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
     f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
     cfg = L.LossConfig(kl_beta=0.1, entropy_coef=0.01)
-    step = grpo.GRPOStep(H, V, cfg, chunk_rows=chunk, recompute=recompute)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=chunk, **MODES[mode])
     res = step(packed, go, rewards, h, W, f(lold), f(lref))
     torch.cuda.synchronize()
     # oracle: logp_new from the LM-head restatement at action rows
