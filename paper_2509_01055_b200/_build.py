@@ -23,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", "-Xptxas", "-v"]
+if os.environ.get("TL_GEMM_STATS") == "1":  # profiling build: GEMM stall counters
+    FLAGS.append("-DTL_GEMM_STATS=1")
 
 
 def _headers() -> list[Path]:

@@ -34,7 +34,27 @@
 
 #include "sm100_ptx.cuh"
 
+// Optional stall accounting (profiling builds only: TL_GEMM_STATS=1, see
+// tools/gemm_stats.py): per CTA, clock64 cycles spent in each wait of the
+// three roles, accumulated into tl::g_gemm_stats[blockIdx.x * 8 + slot].
+#ifndef TL_GEMM_STATS
+#define TL_GEMM_STATS 0
+#endif
+
 namespace tl {
+
+#if TL_GEMM_STATS
+__device__ unsigned long long* g_gemm_stats = nullptr;  // one TU (lmhead.cu) includes this
+enum { ST_PROD_SYNC = 0, ST_PROD_EMPTY, ST_MMA_FULL, ST_MMA_TEMPTY, ST_MMA_TOTAL, ST_EPI_TFULL,
+       ST_EPI_TILE, ST_EPI_END };
+#define TL_STAT_BEGIN(v) const long long v = clock64()
+#define TL_STAT_END(v, slot) \
+  do { if (g_gemm_stats) atomicAdd(g_gemm_stats + blockIdx.x * 8 + (slot), \
+                                   static_cast<unsigned long long>(clock64() - (v))); } while (0)
+#else
+#define TL_STAT_BEGIN(v)
+#define TL_STAT_END(v, slot)
+#endif
 
 constexpr int kBM = 128;  // rows per CTA
 constexpr int kBK = 64;
@@ -58,6 +78,12 @@ struct GemmShape {
   // (unsynchronised they drift apart and re-read operands from HBM 10-18x).
   int* sync_ctr;  // [n_waves], zeroed before launch (NULL = off)
   int sync_every, sync_window;
+  // Serpentine K order: tiles with odd (wave + tile-in-unit) parity stream
+  // their k-blocks last-to-first, so each tile starts on the operand blocks
+  // the previous tile (of this CTA and, in lockstep, of its whole wave) read
+  // last — still in L2 when the operand is too large to stay resident.  Only
+  // the producer's block order changes (fixed per tile: deterministic).
+  int serpentine;
 };
 
 struct UnitCoord {
@@ -99,6 +125,7 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m,
   s.sync_ctr = nullptr;
   s.sync_every = 0;
   s.sync_window = 0;
+  s.serpentine = 0;
   s.m_tiles = (M + kBM * cg - 1) / (kBM * cg);
   s.n_tiles = (N + BN - 1) / BN;
   s.k_blocks = (K + kBK - 1) / kBK;
@@ -199,6 +226,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // sub-MMA j covers tile columns [j*kUmmaN, (j+1)*kUmmaN); this CTA
           // stages rows rank*kBRows.. of each (the pair MMA splits B in half)
           const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
+          const bool rev = shape.serpentine && ((wave + t) & 1);
           for (int kb = 0; kb < shape.k_blocks; ++kb) {
             if (ctr && do_wait && in_step == 0 && sstep >= shape.sync_window) {
               // The lockstep only shapes L2 reuse, never correctness: a wait that
@@ -207,6 +235,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               // published so the other CTAs are not held up either).
               const int need = wave_ctas * (sstep - shape.sync_window + 1);
               int spins = 0;
+              TL_STAT_BEGIN(t_sync);
               while (ld_acquire_gpu(ctr) < need) {
                 __nanosleep(64);
                 if (++spins > (1 << 19)) {
@@ -214,12 +243,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   break;
                 }
               }
+              TL_STAT_END(t_sync, ST_PROD_SYNC);
             }
-            mbar_wait(&empty_bar[stage], phase ^ 1);
+            {
+              TL_STAT_BEGIN(t_e);
+              mbar_wait(&empty_bar[stage], phase ^ 1);
+              TL_STAT_END(t_e, ST_PROD_EMPTY);
+            }
             uint8_t* sa = smem + stage * Smem::kStageBytes;
             uint8_t* sb = sa + Smem::kABytes;
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * Smem::kStageBytes);
-            const int k0 = kb * kBK;
+            const int k0 = (rev ? shape.k_blocks - 1 - kb : kb) * kBK;
             auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, uint64_t pol) {
               if constexpr (CG == 2) tma_load_2d_cg2(m, &full_bar[stage], dst, c0, c1, pol);
               else tma_load_2d(m, &full_bar[stage], dst, c0, c1, pol);
@@ -268,14 +302,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      TL_STAT_BEGIN(t_all);
       for (int u = pair; u < shape.n_units; u += n_pairs) {
         const UnitCoord uc = unit_coord(shape, u);
         for (int t = 0; t < uc.n_count; ++t) {
-          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          {
+            TL_STAT_BEGIN(t_te);
+            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            TL_STAT_END(t_te, ST_MMA_TEMPTY);
+          }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * BN;
           for (int kb = 0; kb < shape.k_blocks; ++kb) {
-            mbar_wait(&full_bar[stage], phase);
+            {
+              TL_STAT_BEGIN(t_f);
+              mbar_wait(&full_bar[stage], phase);
+              TL_STAT_END(t_f, ST_MMA_FULL);
+            }
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * Smem::kStageBytes);
             const uint32_t sb = sa + Smem::kABytes;
@@ -308,6 +351,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      TL_STAT_END(t_all, ST_MMA_TOTAL);
     }
   } else if (warp >= kEpiWarp0) {
     // ---------------------------------------------------------- epilogue --
@@ -321,10 +365,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM + row_in_tile;
       Epi::begin_unit(ep, shape, st, row, uc);
       for (int t = 0; t < uc.n_count; ++t) {
-        mbar_wait(&tfull_bar[acc], acc_phase);
+        {
+          TL_STAT_BEGIN(t_tf);
+          mbar_wait(&tfull_bar[acc], acc_phase);
+          if (lane == 0 && q == 0) TL_STAT_END(t_tf, ST_EPI_TFULL);
+        }
         tc_fence_after();
         const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+        TL_STAT_BEGIN(t_tile);
         Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
+        if (lane == 0 && q == 0) TL_STAT_END(t_tile, ST_EPI_TILE);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -336,7 +386,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           acc_phase ^= 1;
         }
       }
+      TL_STAT_BEGIN(t_end);
       Epi::end_unit(ep, shape, st, row, uc);
+      if (lane == 0 && q == 0) TL_STAT_END(t_end, ST_EPI_END);
     }
   }
 

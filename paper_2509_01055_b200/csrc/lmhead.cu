@@ -100,6 +100,10 @@ int make_ab_maps(CUtensorMap* ma, CUtensorMap* mb, const void* A, bool a_mn, lon
   return make_operand_map(mb, B, b_mn, N, K, ldb, kBN / cg);
 }
 
+#if TL_GEMM_STATS
+unsigned long long* h_stats_base = nullptr;  // [PROF categories][160 CTAs][8]
+#endif
+
 template <int CG, bool A_MN, bool B_MN, class Epi, int BN = kBN>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
                 const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
@@ -136,6 +140,12 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
   const int groups = s.n_units < max_groups ? s.n_units : max_groups;
   lc.gridDim = dim3(groups * CG);
+#if TL_GEMM_STATS
+  if (h_stats_base) {  // stream-ordered: this launch's counters go to its category's block
+    unsigned long long* p = h_stats_base + static_cast<size_t>(prof_cat) * 160 * 8;
+    TL_CUDA_TRY(cudaMemcpyToSymbolAsync(g_gemm_stats, &p, sizeof(p), 0, cudaMemcpyHostToDevice, st));
+  }
+#endif
   TL_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, s, ep));
   count_launch();
   return TL_OK;
@@ -272,44 +282,85 @@ struct EpiLseStats {
     st.y = row < sh.M ? p.targets[row] : -1;
     st.zpol = make_policy(p.z_policy);
   }
-  template <int BN>
-  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
-                              uint32_t taddr) {
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      const int cb = col0 + c;
-      const int nvalid = sh.N - cb;  // columns >= N are padding
-      if (p.zout && row < sh.M) store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid, st.zpol);
-      float cm = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float v = __uint_as_float(r[j]);
-        if (j < nvalid) cm = fmaxf(cm, v);
-      }
-      const int yl = st.y - cb;
+  // One 32-column slice of the row: fp16 store, running max rescale, then
+  // sum e and sum e*z with e = 2^(z*log2e - m*log2e).  Full slices (all but
+  // the vocab tail) take a branch-free path: 3-input max, one SFU op per
+  // logit, split accumulators; the target column is looked up only in the
+  // one slice that holds it.
+  __device__ static __forceinline__ void slice(const Params& p, const GemmShape& sh, State& st,
+                                               int row, int cb, const uint32_t (&r)[32]) {
+    const int nvalid = sh.N - cb;  // columns >= N are padding
+    if (p.zout && row < sh.M)
+      store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid, st.zpol);
+    const int yl = st.y - cb;
+    if (static_cast<unsigned>(yl) < 32u) {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (j == yl) st.zy = __uint_as_float(r[j]);
-      if (cm > st.m) {
-        const float f = exp2f((st.m - cm) * kLog2e);
-        st.s *= f;
-        st.t *= f;
-        st.m = cm;
+    }
+    float cm;
+    if (nvalid >= 32) {
+      float m4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* v = reinterpret_cast<const float*>(r) + 8 * q;
+        m4[q] = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
       }
-      const float mb = st.m * kLog2e;
-      float s = 0.f, t = 0.f;
+      cm = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+    } else {
+      cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) cm = fmaxf(cm, __uint_as_float(r[j]));
+    }
+    if (cm > st.m) {
+      const float f = ex2_ftz((st.m - cm) * kLog2e);
+      st.s *= f;
+      st.t *= f;
+      st.m = cm;
+    }
+    const float mb = st.m * kLog2e;
+    float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
+    if (nvalid >= 32) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+        const float e0 = ex2_ftz(fmaf(v0, kLog2e, -mb)), e1 = ex2_ftz(fmaf(v1, kLog2e, -mb));
+        s0 += e0;
+        s1 += e1;
+        t0 = fmaf(e0, v0, t0);
+        t1 = fmaf(e1, v1, t1);
+      }
+    } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float v = __uint_as_float(r[j]);
-        const float e = j < nvalid ? exp2f(fmaf(v, kLog2e, -mb)) : 0.f;
-        s += e;
-        t = fmaf(e, v, t);
+        const float e = j < nvalid ? ex2_ftz(fmaf(v, kLog2e, -mb)) : 0.f;
+        s0 += e;
+        t0 = fmaf(e, v, t0);
       }
-      st.s += s;
-      st.t += t;
+    }
+    st.s += s0 + s1;
+    st.t += t0 + t1;
+  }
+  // TMEM loads are double-buffered: slice c+1 is in flight while slice c is
+  // reduced (tcgen05.wait::ld waits for all outstanding loads).
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
+                              uint32_t taddr) {
+    static_assert(BN % 64 == 0, "slices are processed in pairs");
+    uint32_t ra[32], rb[32];
+    tmem_ld32(taddr, ra);
+    tmem_ld_wait_regs(ra);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 64) {
+      tmem_ld32(taddr + c + 32, rb);
+      slice(p, sh, st, row, col0 + c, ra);
+      tmem_ld_wait_regs(rb);
+      const bool more = c + 64 < BN;
+      if (more) tmem_ld32(taddr + c + 64, ra);
+      slice(p, sh, st, row, col0 + c + 32, rb);
+      if (more) tmem_ld_wait_regs(ra);
     }
   }
   // Publish this strip's row stats; the CTA that finishes the LAST strip of a
@@ -528,6 +579,7 @@ void sync_override(const char* name, int& every, int& window) {
 // Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr).
 GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* name = nullptr) {
   if (name) sync_override(name, every, window);
+  s.serpentine = env_int("TL_SERPENTINE", 1);
   const int n_pairs = num_sms() / s.cg;
   const int waves = (s.n_units + n_pairs - 1) / n_pairs;
   if (ctr && waves <= kSyncWaves && every > 0) {
@@ -640,6 +692,18 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
 }  // namespace tl
 
 using namespace tl;
+
+// Profiling builds only (not in the public header): point the GEMM stall
+// counters at a device buffer of [grid * 8] u64 (NULL = off).
+extern "C" int tl_debug_gemm_stats(void* buf) {
+#if TL_GEMM_STATS
+  h_stats_base = static_cast<unsigned long long*>(buf);
+  return TL_OK;
+#else
+  (void)buf;
+  return TL_ERR_UNSUPPORTED;
+#endif
+}
 
 extern "C" size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
                                             int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
@@ -857,7 +921,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       // N-complete raster (group_m = 1): all H tiles of an M tile run together
       // so each dS k-block is fetched from HBM once; dS streams (evict first).
       const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
-                                     b.sync + 2 * kSyncWaves, 8, 2, "DH");
+                                     b.sync + 2 * kSyncWaves, 16, 1, "DH");
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
@@ -866,7 +930,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
     const GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
-                                   b.sync + 3 * kSyncWaves, 8, 2, "DW");
+                                   b.sync + 3 * kSyncWaves, 16, 1, "DW");
     EpiStoreF32::Params ep{dweight, H, i > 0 ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };
