@@ -37,6 +37,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "masked GRPO-step tokens/sec (pack+adv+logprob+loss) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "tokens/s"
+# ncu DRAM bytes of one C2 chunk (tools/profile_summary.py) for roofline.traffic
+TRAFFIC_JSON = "r1b_gemm_traffic.json"
 
 
 def _peaks():
@@ -219,6 +221,43 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------- GPU path --
+def micro_batches(cfg, groups, max_tokens: int):
+    """Split a rank's groups (in order) into contiguous micro-batches of at
+    most max_tokens packed tokens (whole groups; at least one group each)."""
+    from paper_2509_01055_b200.synthetic import group_tokens
+
+    toks = group_tokens(cfg, groups)
+    out, cur, n = [], [], 0
+    for gid, t in zip(groups, toks):
+        if cur and n + t > max_tokens:
+            out.append(np.asarray(cur, dtype=np.int64))
+            cur, n = [], 0
+        cur.append(int(gid))
+        n += int(t)
+    if cur:
+        out.append(np.asarray(cur, dtype=np.int64))
+    return out
+
+
+def combine_reports_device(reps, agg: int):
+    """parallel.combine_reports on device tensors (no host sync)."""
+    import torch
+
+    from paper_2509_01055_b200 import parallel
+
+    idx = torch.tensor(parallel._ADDITIVE, device=reps[0].device)
+    tot = reps[0].clone()
+    tot.index_copy_(0, idx, torch.stack([r.index_select(0, idx) for r in reps]).sum(0))
+    masked, groups = tot[2], tot[4]
+    if agg == 1:
+        tot[0] = torch.where(masked > 0, tot[11] / masked.clamp_min(1), 0.0)
+    else:
+        tot[0] = torch.where(groups > 0, tot[11] / groups.clamp_min(1), 0.0)
+    tot[1] = torch.where(masked > 0, tot[8] / masked.clamp_min(1), 0.0)
+    tot[3] = torch.where(masked > 0, tot[9] / masked.clamp_min(1), 0.0)
+    return tot
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -231,6 +270,8 @@ def main():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--chunk-rows", type=int, default=None)
+    ap.add_argument("--max-mb-tokens", type=int, default=7_000_000,
+                    help="largest micro-batch (packed tokens) a rank holds at once")
     ap.add_argument("--mode", default="store", choices=["store", "pipelined", "recompute"],
                     help="LM-head backward schedule (TL_LMHEAD_* in include/toolloop_b200.h); "
                          "store is fastest on a power-capped B200 (DESIGN.md §3)")
@@ -262,54 +303,76 @@ def main():
     n_groups_global = cfg.prompts * world
     work = group_act_tokens(cfg, np.arange(n_groups_global))
     shards = parallel.shard_groups(work, world)
-    wl = make_workload(cfg, group_ids=shards[rank])
     agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
     loss_cfg = LossConfig(epsilon_clip=0.2, kl_beta=0.04, loss_agg=cfg.loss_agg)
     norm_tokens = float(work.sum())
-    H, V, T = cfg.hidden, cfg.vocab, wl.n_tokens
+    H, V = cfg.hidden, cfg.vocab
+    # Micro-batches of whole groups when a rank's hidden + dhidden would not
+    # fit in HBM next to the LM head (C3-C5): each is one call of the fused
+    # step with the step's global normalisers, dW accumulated across them.
+    mb_groups = micro_batches(cfg, shards[rank], args.max_mb_tokens)
+    wls = [make_workload(cfg, group_ids=gids) for gids in mb_groups]
+    T_max = max(w.n_tokens for w in wls)
+    T = sum(w.n_tokens for w in wls)
+    n_act = sum(w.n_act for w in wls)
+    wl = wls[0]
 
-    # device-resident inputs
+    # device-resident inputs (one hidden buffer sized for the largest micro-batch)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    hidden = torch.randn((T, H), device=dev, dtype=torch.bfloat16, generator=g)
+    hidden_buf = torch.randn((T_max, H), device=dev, dtype=torch.bfloat16, generator=g)
     gw = torch.Generator(device=dev).manual_seed(99)  # same W on every rank
     weight = (torch.randn((V, H), device=dev, dtype=torch.float32, generator=gw) * 0.02).to(torch.bfloat16)
-    tab = wl.table
-    dtab = {k: torch.from_numpy(np.ascontiguousarray(getattr(tab, k))).to(dev)
-            for k in ("token_pool", "seg_src_off", "seg_len", "seg_is_action", "traj_seg_off")}
-    lold = torch.from_numpy(wl.logp_old).to(dev)
-    lref = torch.from_numpy(wl.logp_ref).to(dev)
-    rewards = torch.from_numpy(wl.rewards).to(dev)
-    # Realistic behaviour-policy log-probs: the current policy's logp on the
-    # action rows (forward-only fused LM head) plus a small drift, so ratios,
-    # clip fraction and KL sit where a real GRPO step puts them.
-    packed0 = packing.pack_table(tab, device=dev, validate=True, vocab=V, device_inputs=dtab)
-    lp_now, _, _ = grpo.lmhead_logprobs(hidden, weight, packed0.input_ids, rows=packed0.act_idx)
+    TAB_KEYS = ("token_pool", "seg_src_off", "seg_len", "seg_is_action", "traj_seg_off")
     gn = torch.Generator(device=dev).manual_seed(4321 + rank)
-    act_rows = packed0.act_idx.long()
-    lold[act_rows] = lp_now + 0.1 * torch.randn(lp_now.shape, device=dev, generator=gn)
-    lref[act_rows] = lold[act_rows] + 0.05 * torch.randn(lp_now.shape, device=dev, generator=gn)
-    wl.logp_old = lold.cpu().numpy()
-    wl.logp_ref = lref.cpu().numpy()
-    del packed0, lp_now, act_rows
+    mbs = []
+    for w in wls:
+        dtab = {k: torch.from_numpy(np.ascontiguousarray(getattr(w.table, k))).to(dev)
+                for k in TAB_KEYS}
+        lold = torch.from_numpy(w.logp_old).to(dev)
+        lref = torch.from_numpy(w.logp_ref).to(dev)
+        hidden = hidden_buf[:w.n_tokens]
+        # Realistic behaviour-policy log-probs: the current policy's logp on
+        # the action rows (forward-only fused LM head) plus a small drift, so
+        # ratios, clip fraction and KL sit where a real GRPO step puts them.
+        packed0 = packing.pack_table(w.table, device=dev, validate=True, vocab=V, device_inputs=dtab)
+        lp_now, _, _ = grpo.lmhead_logprobs(hidden, weight, packed0.input_ids, rows=packed0.act_idx)
+        act_rows = packed0.act_idx.long()
+        lold[act_rows] = lp_now + 0.1 * torch.randn(lp_now.shape, device=dev, generator=gn)
+        lref[act_rows] = lold[act_rows] + 0.05 * torch.randn(lp_now.shape, device=dev, generator=gn)
+        w.logp_old = lold.cpu().numpy()
+        w.logp_ref = lref.cpu().numpy()
+        del packed0, lp_now, act_rows
+        mbs.append({"wl": w, "dtab": dtab, "lold": lold, "lref": lref, "hidden": hidden,
+                    "rewards": torch.from_numpy(w.rewards).to(dev),
+                    "report": torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)})
     step = grpo.GRPOStep(H, V, loss_cfg, chunk_rows=args.chunk_rows,
                          recompute=args.mode == "recompute", pipelined=args.mode == "pipelined")
-    outputs = {
-        "logp": torch.empty(T, dtype=torch.float32, device=dev),
-        "entropy": torch.empty(T, dtype=torch.float32, device=dev),
-        "dhidden": torch.empty((T, H), dtype=torch.bfloat16, device=dev),
-        "dweight": torch.empty((V, H), dtype=torch.float32, device=dev),
-        "report": torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev),
-    }
+    dhidden_buf = torch.empty((T_max, H), dtype=torch.bfloat16, device=dev)
+    dweight = torch.empty((V, H), dtype=torch.float32, device=dev)
+    logp_buf = torch.empty(T_max, dtype=torch.float32, device=dev)
+    ent_buf = torch.empty(T_max, dtype=torch.float32, device=dev)
 
-    def one_step(device_tab, lo, lr, rw):
-        packed = packing.pack_table(tab, device=dev, validate=False, device_inputs=device_tab)
-        res = step(packed, wl.group_off, rw, hidden, weight, lo, lr,
-                   norm_groups=n_groups_global, norm_tokens=norm_tokens, outputs=outputs,
-                   sync_report=False)
+    def one_step(inputs):
+        """inputs[i] = (device segment table, logp_old, logp_ref, rewards) of micro-batch i"""
+        reps = []
+        for i, (mb, (dt, lo, lr, rw)) in enumerate(zip(mbs, inputs)):
+            w = mb["wl"]
+            packed = packing.pack_table(w.table, device=dev, validate=False, device_inputs=dt)
+            out = {"logp": logp_buf[:w.n_tokens], "entropy": ent_buf[:w.n_tokens],
+                   "dhidden": dhidden_buf[:w.n_tokens], "dweight": dweight,
+                   "report": mb["report"]}
+            res = step(packed, w.group_off, rw, mb["hidden"], weight, lo, lr,
+                       norm_groups=n_groups_global, norm_tokens=norm_tokens, outputs=out,
+                       sync_report=False, accumulate_dweight=i > 0)
+            reps.append(res.report_tensor)
+        rep = reps[0] if len(reps) == 1 else combine_reports_device(reps, agg)
         if world > 1:
-            parallel.allreduce_report(res.report_tensor, agg)
-            parallel.allreduce_grad(res.dweight)
-        return res
+            parallel.allreduce_report(rep, agg)
+            parallel.allreduce_grad(dweight)
+        return rep
+
+    def device_inputs():
+        return [(mb["dtab"], mb["lold"], mb["lref"], mb["rewards"]) for mb in mbs]
 
     def barrier():
         if world > 1:
@@ -317,7 +380,7 @@ def main():
 
     # ---- warm-up
     for _ in range(args.warmup):
-        one_step(dtab, lold, lref, rewards)
+        one_step(device_inputs())
     torch.cuda.synchronize()
     barrier()
 
@@ -329,7 +392,7 @@ def main():
         barrier()
         ev0.record()
         for _ in range(args.steps):
-            res = one_step(dtab, lold, lref, rewards)
+            rep_t = one_step(device_inputs())
         ev1.record()
         torch.cuda.synchronize()
         barrier()
@@ -339,8 +402,8 @@ def main():
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
-    rep = grpo.report_dict(res.report_tensor.cpu())
-    tok_global = torch.tensor([T, wl.n_act], device=dev, dtype=torch.float64)
+    rep = grpo.report_dict(rep_t.cpu())
+    tok_global = torch.tensor([T, n_act], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(tok_global)
     T_all, A_all = (float(x) for x in tok_global.tolist())
@@ -350,7 +413,7 @@ def main():
     prof = {}
     if not args.no_profile:
         _lib.profile_enable(True)
-        one_step(dtab, lold, lref, rewards)
+        one_step(device_inputs())
         torch.cuda.synchronize()
         prof = _lib.profile_read()
         _lib.profile_enable(False)
@@ -359,20 +422,21 @@ def main():
     e2e = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        htab = {k: pin(getattr(tab, k)) for k in dtab}
-        h_lold, h_lref, h_rw = pin(wl.logp_old), pin(wl.logp_ref), pin(wl.rewards)
-        h2d = sum(v.numel() * v.element_size() for v in htab.values()) + \
-            h_lold.numel() * 4 + h_lref.numel() * 4 + h_rw.numel() * 8
+        hosts = [({k: pin(getattr(mb["wl"].table, k)) for k in TAB_KEYS}, pin(mb["wl"].logp_old),
+                  pin(mb["wl"].logp_ref), pin(mb["wl"].rewards)) for mb in mbs]
+        h2d = sum(sum(v.numel() * v.element_size() for v in ht.values()) + lo.numel() * 4 +
+                  lr.numel() * 4 + rw.numel() * 8 for ht, lo, lr, rw in hosts)
         host_rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64).pin_memory()
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            d = {k: v.to(dev, non_blocking=True) for k, v in htab.items()}
-            r = one_step(d, h_lold.to(dev, non_blocking=True), h_lref.to(dev, non_blocking=True),
-                         h_rw.to(dev, non_blocking=True))
-            host_rep.copy_(r.report_tensor, non_blocking=True)
+            inputs = [({k: v.to(dev, non_blocking=True) for k, v in ht.items()},
+                       lo.to(dev, non_blocking=True), lr.to(dev, non_blocking=True),
+                       rw.to(dev, non_blocking=True)) for ht, lo, lr, rw in hosts]
+            r = one_step(inputs)
+            host_rep.copy_(r, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         e1.record()
         torch.cuda.synchronize()
@@ -392,18 +456,18 @@ def main():
         return
 
     peak_s, peak_b, hbm, peak_kind = _peaks()
-    flops_alg = 6.0 * wl.n_act * H * V      # fwd logp (2) + dH (2) + dW (2), action rows only
-    flops_issued = 8.0 * wl.n_act * H * V   # + logits recompute in the backward
+    flops_alg = 6.0 * n_act * H * V      # fwd logp (2) + dH (2) + dW (2), action rows only
+    flops_issued = 8.0 * n_act * H * V   # + logits recompute in the backward
     gemm_ms = sum(prof.get(k, (0, 0))[0] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     gemm_launch = sum(prof.get(k, (0, 0))[1] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     roofline = None
     traffic, traffic_note = None, None
-    tp = ROOT / "profiles" / "r1_gemm_traffic.json"
+    tp = ROOT / "profiles" / TRAFFIC_JSON
     if tp.exists() and cfg.name == "c2":
         tj = json.loads(tp.read_text())
         per_chunk = sum(v["dram_read_GB"] + v["dram_write_GB"]
                         for k, v in tj["per_chunk"].items() if k.startswith("gemm"))
-        traffic = per_chunk * 1e9 * wl.n_act / tj["chunk_rows"]
+        traffic = per_chunk * 1e9 * n_act / tj["chunk_rows"]
         traffic_note = (f"bytes/step = ncu --set full DRAM read+write of the fwd/dH/dW GEMM launches "
                         f"of one {tj['chunk_rows']}-row chunk ({per_chunk:.1f} GB, {tp.name}) x chunks/step; "
                         f"per chunk each GEMM must read W (1.09 GB) and h_c or dS (0.27 / 11.5 GB) once")
@@ -429,7 +493,8 @@ def main():
                    "tokens_per_step": int(T_all), "action_tokens_per_step": int(A_all),
                    "action_tokens_per_s": A_all / (ms / 1e3),
                    "parallelism": f"dp{world} (groups, LPT)", "l2": "inputs >> L2 (hidden is GBs)",
-                   "chunk_rows": step._chunk(wl.n_act), "loss_agg": cfg.loss_agg,
+                   "chunk_rows": step._chunk(max(w.n_act for w in wls)), "loss_agg": cfg.loss_agg,
+                   "micro_batches": len(mbs),
                    "lmhead_mode": args.mode},
         "roofline": roofline,
         "e2e": e2e,

@@ -220,6 +220,10 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
  *    elementwise dS pass runs on an internal side stream concurrently with
  *    chunk i+1's forward GEMM (workspace: tl_lmhead_step_workspace_bytes). */
 #define TL_LMHEAD_STORE_LOGITS_PIPELINED 2
+/* Flag OR-ed into `mode`: dweight += this call's dW instead of dweight = dW
+ * (micro-batches of one optimizer step; pass the step's global norm_groups /
+ * norm_tokens to tl_group_advantages so every micro-batch scales alike). */
+#define TL_LMHEAD_ACCUMULATE_DW 0x100
 /* Workspace for tl_grpo_lmhead_step in `mode` (PIPELINED holds two chunks). */
 size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
                                       int64_t n_tokens, int32_t n_traj, int32_t n_groups,
@@ -228,7 +232,8 @@ size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_
  *   logp_new = LMhead(hidden[act rows]); surrogate (K3 math) fused into the
  *   log-prob epilogue; report; loss = -(objective + entropy_coef * mean
  *   entropy); dhidden = dloss/dhidden (bf16 [T, H], observation rows zeroed),
- *   dweight = dloss/dW (fp32 [V, H], overwritten).  dhidden/dweight NULL =
+ *   dweight = dloss/dW (fp32 [V, H], overwritten; accumulated with
+ *   TL_LMHEAD_ACCUMULATE_DW).  dhidden/dweight NULL =
  *   forward + report only. */
 int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const int32_t* input_ids,
                         const uint8_t* loss_mask, const int32_t* act_idx, int64_t n_act,

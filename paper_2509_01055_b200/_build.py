@@ -25,6 +25,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", "-Xptxas", "-v"]
 if os.environ.get("TL_GEMM_STATS") == "1":  # profiling build: GEMM stall counters
     FLAGS.append("-DTL_GEMM_STATS=1")
+if os.environ.get("TL_STAGES256"):  # tuning build: smem ring depth of 256-wide tiles
+    FLAGS.append(f"-DTL_STAGES256={int(os.environ['TL_STAGES256'])}")
 
 
 def _headers() -> list[Path]:

@@ -167,6 +167,7 @@ N_PROF = 12
 LMHEAD_STORE_LOGITS = 0
 LMHEAD_RECOMPUTE = 1
 LMHEAD_STORE_LOGITS_PIPELINED = 2
+LMHEAD_ACCUMULATE_DW = 0x100
 
 
 def profile_enable(on: bool = True) -> None:

@@ -47,13 +47,23 @@ namespace tl {
 __device__ unsigned long long* g_gemm_stats = nullptr;  // one TU (lmhead.cu) includes this
 enum { ST_PROD_SYNC = 0, ST_PROD_EMPTY, ST_MMA_FULL, ST_MMA_TEMPTY, ST_MMA_TOTAL, ST_EPI_TFULL,
        ST_EPI_TILE, ST_EPI_END };
+// accumulated in registers, flushed once per thread at kernel exit
+#define TL_STAT_DECL long long tl_stat[8] = {0, 0, 0, 0, 0, 0, 0, 0}
 #define TL_STAT_BEGIN(v) const long long v = clock64()
-#define TL_STAT_END(v, slot) \
-  do { if (g_gemm_stats) atomicAdd(g_gemm_stats + blockIdx.x * 8 + (slot), \
-                                   static_cast<unsigned long long>(clock64() - (v))); } while (0)
+#define TL_STAT_END(v, slot) (tl_stat[(slot)] += clock64() - (v))
+#define TL_STAT_FLUSH()                                                                  \
+  do {                                                                                   \
+    unsigned long long* gs = g_gemm_stats;                                               \
+    if (gs)                                                                              \
+      for (int i_ = 0; i_ < 8; ++i_)                                                     \
+        if (tl_stat[i_]) atomicAdd(gs + blockIdx.x * 8 + i_,                            \
+                                   static_cast<unsigned long long>(tl_stat[i_]));         \
+  } while (0)
 #else
+#define TL_STAT_DECL
 #define TL_STAT_BEGIN(v)
 #define TL_STAT_END(v, slot)
+#define TL_STAT_FLUSH()
 #endif
 
 constexpr int kBM = 128;  // rows per CTA
@@ -206,6 +216,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  TL_STAT_DECL;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
@@ -392,6 +403,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
+  TL_STAT_FLUSH();
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();
   else __syncthreads();

@@ -38,7 +38,10 @@ constexpr int kCG = 2;  // 2-CTA (cta_group::2) tiles of 256 x 256
 // dH / dW (long K, light epilogue): 256 x 512 pair tiles (two N=256 UMMAs per
 // k-step, TMEM single-buffered) halve the dS re-reads across N tiles.
 constexpr int kBNWide = 512;
-constexpr int kStages = 6;
+#ifndef TL_STAGES256
+#define TL_STAGES256 6
+#endif
+constexpr int kStages = TL_STAGES256;  // ring depth of the 256-wide tiles (32 KB stages)
 constexpr int kStripsFwd = 6;  // even: a wave covers 2 strips of one M group
 constexpr int kMaxStripsFwd = 64;  // partials capacity (profiling overrides)
 constexpr int kGroupM = 16;
@@ -718,7 +721,7 @@ extern "C" size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hid
   Workspace w{nullptr, 0};
   ChunkWs second{};
   carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true,
-        mode == TL_LMHEAD_STORE_LOGITS_PIPELINED ? &second : nullptr);
+        (mode & ~TL_LMHEAD_ACCUMULATE_DW) == TL_LMHEAD_STORE_LOGITS_PIPELINED ? &second : nullptr);
   return w.used + 1024;
 }
 
@@ -804,12 +807,14 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                    int64_t n_tokens, int32_t H, int32_t V, int32_t n_traj,
                                    int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
                                    float* entropy_out, uint16_t* dhidden, float* dweight,
-                                   double* report, int32_t chunk_rows, int32_t mode,
+                                   double* report, int32_t chunk_rows, int32_t mode_flags,
                                    void* workspace, size_t workspace_bytes, tl_stream_t stream) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
+  const int mode = mode_flags & ~TL_LMHEAD_ACCUMULATE_DW;
+  const bool acc_dw = (mode_flags & TL_LMHEAD_ACCUMULATE_DW) != 0;
   TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE ||
                  mode == TL_LMHEAD_STORE_LOGITS_PIPELINED,
-             TL_ERR_INVALID_ARG, "unknown lmhead mode %d", mode);
+             TL_ERR_INVALID_ARG, "unknown lmhead mode %d", mode_flags);
   TL_REQUIRE(cfg->use_mask == 1, TL_ERR_UNSUPPORTED, "LM-head step computes action rows only");
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(H > 0 && V > 0 && chunk_rows > 0 && n_act >= 0, TL_ERR_INVALID_ARG, "bad sizes");
@@ -842,7 +847,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       count_launch();
     }
   }
-  if (bwd && n_act == 0) {
+  if (bwd && n_act == 0 && !acc_dw) {
     cudaMemsetAsync(dweight, 0, static_cast<size_t>(V) * H * sizeof(float), st);
   }
 
@@ -931,7 +936,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
     const GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
                                    b.sync + 3 * kSyncWaves, 16, 1, "DW");
-    EpiStoreF32::Params ep{dweight, H, i > 0 ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
+    EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };
 

@@ -143,7 +143,12 @@ class GRPOStep:
     def __call__(self, packed: PackedBatch, group_off, rewards, hidden, weight, logp_old,
                  logp_ref=None, *, backward: bool = True, norm_groups: float | None = None,
                  norm_tokens: float | None = None, stream=None, outputs=None,
-                 adv_cache=None, sync_report: bool = True) -> StepResult:
+                 adv_cache=None, sync_report: bool = True,
+                 accumulate_dweight: bool = False) -> StepResult:
+        """One step over `packed`.  Micro-batching an optimizer step: call once
+        per micro-batch with the step's global norm_groups / norm_tokens and
+        accumulate_dweight=True after the first (outputs["dweight"] reused),
+        then combine the reports with parallel.combine_reports."""
         import torch
 
         L = _lib.lib()
@@ -199,7 +204,9 @@ class GRPOStep:
             packed.traj_of_token.data_ptr(), packed.cu_seqlens.data_ptr(), d_go.data_ptr(),
             logp_old.data_ptr(), _lib.ptr(logp_ref), adv32.data_ptr(), traj_w.data_ptr(), T,
             self.H, self.V, packed.n_traj, n_groups, c, logp.data_ptr(), ent.data_ptr(),
-            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk, self.mode, ws.data_ptr(), ws_bytes,
+            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk,
+            self.mode | (_lib.LMHEAD_ACCUMULATE_DW if accumulate_dweight else 0), ws.data_ptr(),
+            ws_bytes,
             _lib.stream_handle(stream)))
         return StepResult(report=report_dict(rep.cpu()) if sync_report else {}, report_tensor=rep, logp=logp[:T], entropy=ent[:T],
                           dhidden=dh, dweight=dw, adv=adv64)

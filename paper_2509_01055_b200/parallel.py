@@ -49,6 +49,16 @@ def finalize_report(rep: np.ndarray, agg: int = 0) -> np.ndarray:
     return rep
 
 
+def combine_reports(reports, agg: int = 0) -> np.ndarray:
+    """Reports of disjoint micro-batches (or ranks) of one step -> the step's
+    report: sum the additive partials, recompute the ratios."""
+    reps = [np.asarray(r, dtype=np.float64) for r in reports]
+    tot = reps[0].copy()
+    for r in reps[1:]:
+        tot[list(_ADDITIVE)] += r[list(_ADDITIVE)]
+    return finalize_report(tot, agg)
+
+
 def allreduce_report(rep_tensor, agg: int = 0, group=None):
     """N1: sum the additive report fields over ranks (in place) and recompute
     the ratios.  Works for NCCL (device tensor) and gloo (CPU tensor)."""

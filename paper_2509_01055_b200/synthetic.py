@@ -91,6 +91,12 @@ def group_act_tokens(cfg: WorkloadConfig, group_ids, seed: int | None = None) ->
     return np.asarray([_group_shape(cfg, int(g), seed)[1] for g in group_ids])
 
 
+def group_tokens(cfg: WorkloadConfig, group_ids, seed: int | None = None) -> np.ndarray:
+    """Packed-token count per group (action + observation) without ids."""
+    return np.asarray([sum(int(l.sum()) for l in _group_shape(cfg, int(g), seed)[0])
+                       for g in group_ids])
+
+
 def _group_shape(cfg: WorkloadConfig, g: int, seed: int | None):
     rng = np.random.default_rng([SEED0 if seed is None else seed, g])
     segs = []

@@ -456,3 +456,50 @@ def test_grpo_lmhead_step_dapo_token_mean():
     dH, dW = LH.lmhead_backward(hn[act], Wn, ids[act], -grads[act] / len(act))
     assert _rel_fro(res.dhidden.float().cpu().numpy()[act], dH) <= 2e-2
     assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
+
+
+@pytest.mark.parametrize("agg", ["seq-mean-token-mean", "token-mean"])
+def test_microbatched_step_matches_full_batch(agg):
+    """An optimizer step split into micro-batches of whole groups (global
+    normalisers, dW accumulated with TL_LMHEAD_ACCUMULATE_DW, reports combined
+    from additive partials) equals the one-shot step: per-row outputs
+    bitwise, dW to fp32 accumulation order, the report to fp64 rounding."""
+    from paper_2509_01055_b200 import parallel
+
+    H, V = 128, 1000
+    trajs, rewards, go, _, lold, lref = _synthetic_batch(9, n_groups=8, G=4)
+    for tr in trajs:
+        for i, (o, toks) in enumerate(tr):
+            tr[i] = (o, [t % V for t in toks])
+    packed = packing.pack([_traj(s) for s in trajs])
+    T, n_act = packed.n_tokens, packed.n_act
+    g = torch.Generator(device="cuda").manual_seed(23)
+    h = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    lo, lr = f(lold), f(lref)
+    cfg = L.LossConfig(kl_beta=0.05, entropy_coef=0.01, loss_agg=agg)
+    agg_i = 1 if agg == "token-mean" else 0
+    full = grpo.GRPOStep(H, V, cfg, chunk_rows=256)(packed, go, rewards, h, W, lo, lr)
+    # three micro-batches of whole groups: groups [0,3), [3,5), [5,8)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=256)
+    dw = torch.empty(V, H, dtype=torch.float32, device="cuda")
+    cu = packed.cu_seqlens.cpu().numpy()
+    reps, dhs, lps = [], [], []
+    for i, (g0, g1) in enumerate([(0, 3), (3, 5), (5, 8)]):
+        b0, b1 = int(go[g0]), int(go[g1])
+        t0, t1 = int(cu[b0]), int(cu[b1])
+        pk = packing.pack([_traj(s) for s in trajs[b0:b1]])
+        r = step(pk, go[g0:g1 + 1] - go[g0], rewards[b0:b1], h[t0:t1].contiguous(), W,
+                 lo[t0:t1].contiguous(), lr[t0:t1].contiguous(), norm_groups=len(go) - 1,
+                 norm_tokens=n_act, outputs={"dweight": dw}, accumulate_dweight=i > 0)
+        reps.append(r.report_tensor.cpu().numpy())
+        dhs.append(r.dhidden.clone())
+        lps.append(r.logp.clone())
+    assert torch.equal(torch.cat(lps), full.logp)
+    assert torch.equal(torch.cat(dhs), full.dhidden)
+    assert _rel_fro(dw.cpu().numpy(), full.dweight.cpu().numpy()) <= 1e-6
+    rep = parallel.combine_reports(reps, agg_i)
+    ref = full.report_tensor.cpu().numpy()
+    assert rep[2] == ref[2] and rep[4] == ref[4] and rep[5] == ref[5]
+    np.testing.assert_allclose(rep, ref, rtol=1e-9, atol=1e-12)
