@@ -462,8 +462,10 @@ def test_grpo_lmhead_step_dapo_token_mean():
 def test_microbatched_step_matches_full_batch(agg):
     """An optimizer step split into micro-batches of whole groups (global
     normalisers, dW accumulated with TL_LMHEAD_ACCUMULATE_DW, reports combined
-    from additive partials) equals the one-shot step: per-row outputs
-    bitwise, dW to fp32 accumulation order, the report to fp64 rounding."""
+    from additive partials) equals the one-shot step to accumulation order:
+    a row's tile may sit at another wave parity (serpentine K order), so
+    per-row outputs agree to fp32 / one bf16 ulp, dW to fp32 accumulation
+    order, the report to fp64 rounding."""
     from paper_2509_01055_b200 import parallel
 
     H, V = 128, 1000
@@ -496,8 +498,9 @@ def test_microbatched_step_matches_full_batch(agg):
         reps.append(r.report_tensor.cpu().numpy())
         dhs.append(r.dhidden.clone())
         lps.append(r.logp.clone())
-    assert torch.equal(torch.cat(lps), full.logp)
-    assert torch.equal(torch.cat(dhs), full.dhidden)
+    torch.testing.assert_close(torch.cat(lps), full.logp, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(torch.cat(dhs).float(), full.dhidden.float(), rtol=2 ** -7,
+                               atol=1e-8)
     assert _rel_fro(dw.cpu().numpy(), full.dweight.cpu().numpy()) <= 1e-6
     rep = parallel.combine_reports(reps, agg_i)
     ref = full.report_tensor.cpu().numpy()
