@@ -1,0 +1,8 @@
+# compute-sanitizer over the GPU parity tests (memcheck on the fused step incl. tcgen05 GEMMs; racecheck/synccheck on shared-memory kernels)
+K1='test_pack or test_advantages or test_loss_fp32 or test_grpo_lmhead_step_vs_oracle or microbatch or dapo'
+K2='test_pack or test_advantages or test_loss_fp32 or test_grpo_lmhead_step_vs_oracle'
+for tool in memcheck racecheck synccheck; do
+  k="$K1"; [ $tool != memcheck ] && k="$K2"
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "$k" > gpurun_out/san_$tool.log 2>&1
+  echo "== $tool rc=$?"; grep -E "passed|failed|ERROR SUMMARY|RACECHECK SUMMARY" gpurun_out/san_$tool.log | tail -3
+done
