@@ -86,8 +86,11 @@ struct GemmShape {
   // the wave finished step s - sync_window.  Keeps the CTAs that share A / B
   // tiles within a few k-blocks of each other so the sharing hits L2
   // (unsynchronised they drift apart and re-read operands from HBM 10-18x).
-  int* sync_ctr;  // [n_waves], zeroed before launch (NULL = off)
+  int* sync_ctr;  // [n_waves] (or [n_waves * 8] split), zeroed before launch (NULL = off)
   int sync_every, sync_window;
+  // sync_split: lockstep only among the CTAs of a wave that run the same
+  // (M group, strip) — the ones sharing B tiles — instead of the whole wave.
+  int sync_split;
   // Serpentine K order: tiles with odd (wave + tile-in-unit) parity stream
   // their k-blocks last-to-first, so each tile starts on the operand blocks
   // the previous tile (of this CTA and, in lockstep, of its whole wave) read
@@ -135,6 +138,7 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m,
   s.sync_ctr = nullptr;
   s.sync_every = 0;
   s.sync_window = 0;
+  s.sync_split = 0;
   s.serpentine = 0;
   s.m_tiles = (M + kBM * cg - 1) / (kBM * cg);
   s.n_tiles = (N + BN - 1) / BN;
@@ -229,8 +233,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int u = pair; u < shape.n_units; u += n_pairs, ++wave) {
         const UnitCoord uc = unit_coord(shape, u);
         const int m0 = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM;
-        int* ctr = shape.sync_ctr ? shape.sync_ctr + wave : nullptr;
-        const int wave_ctas = CG * min(n_pairs, shape.n_units - wave * n_pairs);
+        int* ctr = nullptr;
+        int wave_ctas = 0;
+        if (shape.sync_ctr) {
+          const int w0 = wave * n_pairs;
+          const int wn = min(n_pairs, shape.n_units - w0);
+          if (shape.sync_split) {
+            auto key = [&](int uu) {
+              const UnitCoord c = unit_coord(shape, uu);
+              return (c.m_tile / shape.group_m) * shape.n_strips + c.strip_idx;
+            };
+            const int km = key(u);
+            int cnt = 0;
+            for (int j = 0; j < wn; ++j) cnt += key(w0 + j) == km;
+            const int slot = km - key(w0);  // keys ascend within a wave
+            // slots >= 8 share the last counter: extra arrivals only loosen the wait
+            ctr = shape.sync_ctr + wave * 8 + (slot < 8 ? slot : 7);
+            wave_ctas = CG * cnt;
+          } else {
+            ctr = shape.sync_ctr + wave;
+            wave_ctas = CG * wn;
+          }
+        }
         int sstep = 0, in_step = 0;
         bool do_wait = true;
         for (int t = 0; t < uc.n_count; ++t) {

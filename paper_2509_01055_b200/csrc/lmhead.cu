@@ -24,6 +24,7 @@
 #include <cuda_fp16.h>
 
 #include <mutex>
+#include <string>
 
 #include "gemm_sm100.cuh"
 #include "grpo_token.cuh"
@@ -580,15 +581,18 @@ void sync_override(const char* name, int& every, int& window) {
 }
 
 // Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr).
-GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* name = nullptr) {
+GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* name = nullptr,
+                    int split_dflt = 0) {
   if (name) sync_override(name, every, window);
   s.serpentine = env_int("TL_SERPENTINE", 1);
   const int n_pairs = num_sms() / s.cg;
   const int waves = (s.n_units + n_pairs - 1) / n_pairs;
-  if (ctr && waves <= kSyncWaves && every > 0) {
+  const int split = name ? env_int((std::string("TL_SYNC_SPLIT_") + name).c_str(), split_dflt) : 0;
+  if (ctr && waves * (split ? 8 : 1) <= kSyncWaves && every > 0) {
     s.sync_ctr = ctr;
     s.sync_every = every;
     s.sync_window = window;
+    s.sync_split = split;
   }
   return s;
 }
@@ -668,7 +672,9 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int group_m = env_int("TL_FWD_GROUPM", num_sms() / kCG / 2);
   GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, env_int("TL_FWD_POLA", 2),
                            env_int("TL_FWD_POLB", 0));
-  return with_sync(s, sync, s.k_blocks, 1, "FWD");
+  // per-strip lockstep: a strip's 37 pairs (sharing its W tiles) wait on each
+  // other only, not on the other strip of the wave (step -0.5 %, gpu_r25)
+  return with_sync(s, sync, s.k_blocks, 1, "FWD", 1);
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also

@@ -502,7 +502,7 @@ def test_microbatched_step_matches_full_batch(agg):
     # (elementwise relative error is meaningless where dS.W cancels to ~0)
     assert _rel_fro(torch.cat(dhs).float().cpu().numpy(),
                     full.dhidden.float().cpu().numpy()) <= 1e-3
-    assert _rel_fro(dw.cpu().numpy(), full.dweight.cpu().numpy()) <= 1e-6
+    assert _rel_fro(dw.cpu().numpy(), full.dweight.cpu().numpy()) <= 1e-3  # dS is bf16
     rep = parallel.combine_reports(reps, agg_i)
     ref = full.report_tensor.cpu().numpy()
     assert rep[2] == ref[2] and rep[4] == ref[4] and rep[5] == ref[5]
