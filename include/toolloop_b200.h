@@ -268,6 +268,35 @@ int tl_ingest_fill(const tl_episode_batch* batch, int32_t* token_pool, int32_t* 
                    double* logp_ref);
 void tl_ingest_free(tl_episode_batch* batch);
 
+/* ------------------------------------------------------------------------
+ * F4 — incremental tokenisation of rollout segments (host, multithreaded C++).
+ * Replaces tokenizer.ToyMergeTokenizer (tokenizer.py:36-87: byte ids 0..255,
+ * ordered merge table, rule k -> id 256+k, one left-to-right pass per rule)
+ * applied segment by segment with the token cap of trajectory._tokenize
+ * (trajectory.py:97-104) / orchestrator.feed_action, feed_response
+ * (orchestrator.py:112-117, :156-161).
+ * ---------------------------------------------------------------------- */
+typedef struct tl_tokenizer tl_tokenizer;
+/* Merge k = (left, right) byte strings: left = merge_bytes[off[2k], off[2k+1]),
+ * right = merge_bytes[off[2k+1], off[2k+2]).  Both must already be tokens
+ * (TL_ERR_INVALID_ARG otherwise, tokenizer.py:55-58 ValueError). */
+int tl_tokenizer_create(const uint8_t* merge_bytes, const int64_t* merge_off, int32_t n_merges,
+                        tl_tokenizer** out);
+void tl_tokenizer_free(tl_tokenizer* tok);
+int32_t tl_tokenizer_vocab_size(const tl_tokenizer* tok);
+/* Encode segment i = text[text_off[i], text_off[i+1]) on its own (never across
+ * a segment boundary), keep its first max_tokens[i] ids (max_tokens NULL or
+ * < 0: no cap).  Ids go to token_pool[text_off[i] ...] (never more ids than
+ * bytes), so (token_pool, seg_src_off = text_off, seg_len) is directly the
+ * segment table of tl_pack_varlen.  n_threads <= 0: all hardware threads. */
+int tl_tokenize_segments(const tl_tokenizer* tok, const uint8_t* text, const int64_t* text_off,
+                         int64_t n_segments, const int32_t* max_tokens, int32_t* token_pool,
+                         int32_t* seg_len, int32_t n_threads);
+/* Bytes of ids[0..n) (ToyMergeTokenizer.decode before UTF-8 decoding): *len =
+ * total bytes; copied into out only if they fit in cap (out NULL: size only). */
+int tl_tokenizer_decode(const tl_tokenizer* tok, const int32_t* ids, int64_t n, uint8_t* out,
+                        int64_t cap, int64_t* len);
+
 /* Plain tcgen05 GEMM (building block, exported for tests):
  * C[M,N] (+)= A[M,K] * B[N,K]^T with A given K-major ([M,K], lda) or MN-major
  * ([K,M], lda) and B K-major ([N,K], ldb) or MN-major ([K,N], ldb).

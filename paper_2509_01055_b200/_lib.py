@@ -38,6 +38,8 @@ EXPORTS = [
     "tl_grpo_lmhead_step",
     "tl_gemm_bf16",
     "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
+    "tl_tokenizer_create", "tl_tokenizer_free", "tl_tokenizer_vocab_size",
+    "tl_tokenize_segments", "tl_tokenizer_decode",
 ]
 
 
@@ -97,6 +99,11 @@ _SIGS = {
                                   C.POINTER(_I64), C.POINTER(_I32)]),
     "tl_ingest_fill": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tl_ingest_free": (None, [_P]),
+    "tl_tokenizer_create": (C.c_int, [_P, _P, _I32, C.POINTER(C.c_void_p)]),
+    "tl_tokenizer_free": (None, [_P]),
+    "tl_tokenizer_vocab_size": (_I32, [_P]),
+    "tl_tokenize_segments": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P, _I32]),
+    "tl_tokenizer_decode": (C.c_int, [_P, _P, _I64, _P, _I64, C.POINTER(_I64)]),
 }
 
 _lock = threading.Lock()

@@ -12,6 +12,8 @@ output of the reference's own functions:
                     grpo_single_turn_loss, unclipped_objective, token_ratio}
   toolloop.trajectory.{flatten, action_mask} over ToyMergeTokenizer ids
   toolloop.cli `loss` report over an episode log (+ sidecar)
+  toolloop.tokenizer.ToyMergeTokenizer / trajectory._tokenize (tokenizer.json;
+  `--only tokenizer` regenerates just that file)
 """
 
 from __future__ import annotations
@@ -238,7 +240,46 @@ def gen_cli_report():
     }
 
 
+# --------------------------------------------------------------- tokenizer ----
+
+def gen_tokenizer():
+    """ToyMergeTokenizer.encode / decode and trajectory._tokenize (token cap)
+    over fuzzed texts (ASCII tool markup + multi-byte characters) for several
+    merge tables, plus the tables the reference rejects."""
+    from toolloop.trajectory import _tokenize
+
+    rng = random.Random(2509)
+    alphabet = "abcdefr <>/\n`otuhpyns" + "πé≈—\u00a0"
+    tables = [None, [], [["a", "b"]], [["a", "b"], ["ab", "c"]],
+              [["<", "/"], ["</", "r"], ["e", "r"], ["er", ">"], [">", "\n"], ["\n", "\n"]]]
+    cases = []
+    for ti, merges in enumerate(tables):
+        tok = ToyMergeTokenizer() if merges is None else ToyMergeTokenizer([tuple(m) for m in merges])
+        for _ in range(150):
+            text = "".join(rng.choice(alphabet) for _ in range(rng.randrange(0, 120)))
+            cap = rng.choice([None, 0, 1, 3, 10, 40])
+            t_text, t_ids = _tokenize(tok, text, cap)
+            cases.append({"table": ti, "text": text, "ids": tok.encode(text), "cap": cap,
+                          "cap_text": t_text, "cap_ids": t_ids})
+        cases.append({"table": ti, "text": "", "ids": tok.encode(""), "cap": None,
+                      "cap_text": "", "cap_ids": []})
+    rejected = []
+    for merges in ([["ab", "c"]], [["a", "b"], ["abc", "d"]], [["é", "a"]]):
+        try:
+            ToyMergeTokenizer([tuple(m) for m in merges])
+        except ValueError as e:
+            rejected.append({"merges": merges, "error": str(e)})
+    return {"tables": tables, "vocab_sizes": [
+        (ToyMergeTokenizer() if m is None else ToyMergeTokenizer([tuple(x) for x in m])).vocab_size
+        for m in tables], "cases": cases, "rejected": rejected}
+
+
 def main() -> None:
+    if "--only" in sys.argv:  # regenerate one fixture, leave the others untouched
+        which = sys.argv[sys.argv.index("--only") + 1]
+        gen = {"tokenizer": gen_tokenizer}[which]
+        (HERE / f"{which}.json").write_text(json.dumps(gen()))
+        return
     adv = gen_advantages()
     losses, ratios = gen_losses()
     pack = gen_pack()
@@ -247,6 +288,7 @@ def main() -> None:
     (HERE / "losses.json").write_text(json.dumps({"cases": losses, "ratios": ratios}))
     (HERE / "pack.json").write_text(json.dumps(pack))
     (HERE / "cli_report.json").write_text(json.dumps(cli))
+    (HERE / "tokenizer.json").write_text(json.dumps(gen_tokenizer()))
     for p in sorted(HERE.glob("*.json")):
         print(p.name, p.stat().st_size, "bytes", file=sys.stderr)
 

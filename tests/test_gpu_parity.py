@@ -507,3 +507,27 @@ def test_microbatched_step_matches_full_batch(agg):
     ref = full.report_tensor.cpu().numpy()
     assert rep[2] == ref[2] and rep[4] == ref[4] and rep[5] == ref[5]
     np.testing.assert_allclose(rep, ref, rtol=1e-9, atol=1e-12)
+
+
+def test_texts_to_device_batch():
+    """F4 -> K1: rollout texts tokenised segment by segment in one native call,
+    packed on the device; ids / mask equal flatten / action_mask of the
+    per-segment encodings (oracle)."""
+    import random
+
+    from oracle import tokenizer_oracle as TO
+    from paper_2509_01055_b200 import tokenizer as TK
+
+    rng = random.Random(5)
+    tok = TK.ToyMergeTokenizer()
+    trajs = []
+    for _ in range(64):
+        k = rng.randrange(0, 5)
+        trajs.append([("action" if s % 2 == 0 else "observation",
+                       "".join(rng.choice("ab</>\nerx é") for _ in range(rng.randrange(1, 50))))
+                      for s in range(2 * k + 1)])
+    tab = TK.segment_table(tok, trajs, max_tokens=24)
+    got = packing.pack_table(tab)
+    ref = P.pack_varlen([[(o, TO.tokenize(t, 24)[1]) for o, t in segs] for segs in trajs])
+    for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "act_idx"):
+        assert np.array_equal(getattr(got, k).cpu().numpy(), ref[k]), k
