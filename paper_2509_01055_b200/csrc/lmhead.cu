@@ -44,7 +44,7 @@ constexpr int kBNWide = 512;
 #endif
 constexpr int kStages = TL_STAGES256;  // ring depth of the 256-wide tiles (32 KB stages)
 constexpr int kStripsFwd = 6;  // even: a wave covers 2 strips of one M group
-constexpr int kMaxStripsFwd = 64;  // partials capacity (profiling overrides)
+constexpr int kMaxStripsFwd = 16;  // partials capacity (TL_FWD_STRIPS profiling override)
 constexpr int kGroupM = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 
