@@ -39,17 +39,20 @@ def bf16_from_bits(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-def lmhead_forward(h: np.ndarray, W: np.ndarray, y: np.ndarray, chunk: int = 512):
+def lmhead_forward(h: np.ndarray, W: np.ndarray, y: np.ndarray, chunk: int = 512,
+                   exact: bool = False):
     """h [T, H] fp32 (bf16 values), W [V, H] fp32 (bf16 values), y [T] int.
-    Returns logp, ent, lse (fp64 [T])."""
+    Returns logp, ent, lse (fp64 [T]).  exact=True forms the logits in fp64
+    (bf16 products are exact in fp64), so the only error left is the GPU's."""
     T = h.shape[0]
     logp = np.empty(T)
     ent = np.empty(T)
     lse = np.empty(T)
-    Wt = np.ascontiguousarray(W.T)
+    Wt = np.ascontiguousarray(W.T, dtype=np.float64 if exact else W.dtype)
     for s in range(0, T, chunk):
         e = min(T, s + chunk)
-        z = (h[s:e] @ Wt).astype(np.float64)
+        hs = h[s:e].astype(np.float64) if exact else h[s:e]
+        z = (hs @ Wt).astype(np.float64)
         m = z.max(axis=1, keepdims=True)
         ex = np.exp(z - m)
         se = ex.sum(axis=1, keepdims=True)
