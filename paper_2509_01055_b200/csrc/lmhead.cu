@@ -487,37 +487,53 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t
 
 // In place: fp16 logits z (written by the forward epilogue) -> bf16
 // dS = g (onehot(y) - p) - c p (z - E_p z), p = exp(z - lse).  One CTA per row.
+// dS for 8 logits held as fp16 in one 16-byte word:
+//   d = -g p - c p (z - E_p z) = p (A + B z),  A = c E_p z - g,  B = -c,
+//   p = 2^(z log2e - lse log2e)  (one FFMA + one SFU op per logit),
+// plus g at the target column (the one word that holds it).
+__device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float l2, float A, float B, int yy,
+                                           float gg) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  float d[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 z = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    d[2 * k] = ex2_ftz(fmaf(z.x, kLog2e, -l2)) * fmaf(B, z.x, A);
+    d[2 * k + 1] = ex2_ftz(fmaf(z.y, kLog2e, -l2)) * fmaf(B, z.y, A);
+  }
+  const int yl = yy - col0;
+  if (static_cast<unsigned>(yl) < 8u) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == yl) d[j] += gg;
+  }
+  return make_uint4(pack_bf16x2(d[0], d[1]), pack_bf16x2(d[2], d[3]), pack_bf16x2(d[4], d[5]),
+                    pack_bf16x2(d[6], d[7]));
+}
+
 // Rows are grid-strided: one CTA per row when launched alone, or a small
 // persistent grid when it runs beside the next chunk's forward GEMM
-// (pipelined mode) and should trickle at low HBM intensity.
+// (pipelined mode) and should trickle at low HBM intensity.  Two 16-byte
+// words in flight per thread (the pass is HBM-bound; in the step it runs at
+// the power-capped SM clock, so it is also kept short in instructions).
 __global__ void __launch_bounds__(256)
     dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec, int V, int rows,
                             const int32_t* __restrict__ y, const float* __restrict__ lse,
                             const float* __restrict__ g, const float* __restrict__ c,
                             const float* __restrict__ ez) {
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-  const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r], e = ez[r];
-  const int yy = y[r];
-  uint4* row = buf + static_cast<long long>(r) * ld_vec;
-  const int nvec = (V + 7) / 8;
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    const uint4 q = row[v];
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const __half2 h2 = *reinterpret_cast<const __half2*>(&w[k]);
-      const float2 z = __half22float2(h2);
-      const int col = v * 8 + 2 * k;
-      const float p0 = exp2f(fmaf(z.x, kLog2e, -l2)), p1 = exp2f(fmaf(z.y, kLog2e, -l2));
-      float d0 = -gg * p0 - cc * p0 * (z.x - e);
-      float d1 = -gg * p1 - cc * p1 * (z.y - e);
-      if (col == yy) d0 += gg;
-      if (col + 1 == yy) d1 += gg;
-      o[k] = pack_bf16x2(d0, d1);
+    const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r];
+    const float A = cc * ez[r] - gg, B = -cc;
+    const int yy = y[r];
+    uint4* row = buf + static_cast<long long>(r) * ld_vec;
+    const int nvec = (V + 7) / 8;
+    int v = threadIdx.x;
+    for (; v + static_cast<int>(blockDim.x) < nvec; v += 2 * blockDim.x) {
+      const uint4 q0 = row[v], q1 = row[v + blockDim.x];
+      row[v] = dsoftmax8(q0, v * 8, l2, A, B, yy, gg);
+      row[v + blockDim.x] = dsoftmax8(q1, (v + blockDim.x) * 8, l2, A, B, yy, gg);
     }
-    row[v] = make_uint4(o[0], o[1], o[2], o[3]);
-  }
+    if (v < nvec) row[v] = dsoftmax8(row[v], v * 8, l2, A, B, yy, gg);
   }
 }
 
