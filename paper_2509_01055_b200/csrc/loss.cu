@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ lref, const uint8_t* __restrict__ mask,
                        const int32_t* __restrict__ cu, const float* __restrict__ adv,
                        const float* __restrict__ traj_w, tl_loss_config cfg,
-                       float* __restrict__ grad, double* __restrict__ traj_out) {
+                       float* __restrict__ grad, double* __restrict__ traj_out, int vec_ok) {
   constexpr int kV = 5;
   __shared__ double sh[kV][256 / 32];
   const int b = blockIdx.x;
@@ -324,21 +324,47 @@ __global__ void __launch_bounds__(256)
   const float lo = static_cast<float>(1.0 - cfg.eps_low), hi = static_cast<float>(1.0 + cfg.eps_high);
   const float beta = static_cast<float>(cfg.kl_beta);
   double v[kV] = {0, 0, 0, 0, 0};  // term, k3, n_act, clipped, clamps
-#pragma unroll 4
-  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-    if (cfg.use_mask && !mask[t]) {
-      if (grad) grad[t] = 0.f;
-      continue;
-    }
-    const float rf = cfg.has_ref ? lref[t] : 0.f;
-    const TokTermF o = grpo_token_f32(lnew[t], lold[t], rf, cfg.has_ref != 0 && rf == rf, a, lo,
-                                      hi, beta, cfg.objective);
-    if (grad) grad[t] = o.dterm * wt;
+  auto one = [&](int t, float ln, float lf, float rf, bool act) -> float {
+    if (!act) return 0.f;
+    const TokTermF o = grpo_token_f32(ln, lf, rf, cfg.has_ref != 0 && rf == rf, a, lo, hi, beta,
+                                      cfg.objective);
     v[0] += o.term;
     v[1] += o.k3;
     v[2] += 1.0;
     v[3] += (o.flags & kFlagClipped) ? 1.0 : 0.0;
     v[4] += (o.flags & kFlagClamped) ? 1.0 : 0.0;
+    return o.dterm * wt;
+  };
+  auto scalar = [&](int t) {
+    const bool act = !cfg.use_mask || mask[t];
+    const float g = act ? one(t, lnew[t], lold[t], cfg.has_ref ? lref[t] : 0.f, true) : 0.f;
+    if (grad) grad[t] = g;
+  };
+  // 16-byte vectors over the 4-aligned body (observation runs skip their
+  // log-prob loads), scalar head / tail: trajectories start anywhere.
+  const int b0 = (t0 + 3) & ~3, b1 = t1 & ~3;
+  if (!vec_ok || b0 >= b1) {
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) scalar(t);
+  } else {
+    if (t0 + static_cast<int>(threadIdx.x) < b0) scalar(t0 + threadIdx.x);
+    if (b1 + static_cast<int>(threadIdx.x) < t1) scalar(b1 + threadIdx.x);
+#pragma unroll 2
+    for (int t = b0 + 4 * threadIdx.x; t < b1; t += 4 * blockDim.x) {
+      const uchar4 m = cfg.use_mask ? *reinterpret_cast<const uchar4*>(mask + t)
+                                    : make_uchar4(1, 1, 1, 1);
+      float4 gr = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m.x | m.y | m.z | m.w) {
+        const float4 ln = *reinterpret_cast<const float4*>(lnew + t);
+        const float4 lf = *reinterpret_cast<const float4*>(lold + t);
+        const float4 rf = cfg.has_ref ? *reinterpret_cast<const float4*>(lref + t)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        gr.x = one(t, ln.x, lf.x, rf.x, m.x);
+        gr.y = one(t + 1, ln.y, lf.y, rf.y, m.y);
+        gr.z = one(t + 2, ln.z, lf.z, rf.z, m.z);
+        gr.w = one(t + 3, ln.w, lf.w, rf.w, m.w);
+      }
+      if (grad) *reinterpret_cast<float4*>(grad + t) = gr;
+    }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -506,8 +532,11 @@ extern "C" int tl_loss_f32(const float* logp_new, const float* logp_old, const f
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   tl::ProfScope prof(tl::PROF_LOSS, st);
   if (n_traj > 0) {
+    auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+    const int vec_ok = al(logp_new, 16) && al(logp_old, 16) && al(logp_ref, 16) &&
+                       al(grad, 16) && al(mask, 4);  // NULL pointers are aligned
     tl::loss32_traj_kernel<<<n_traj, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, cu_seqlens,
-                                                   adv32, traj_w, *cfg, grad, traj_out);
+                                                   adv32, traj_w, *cfg, grad, traj_out, vec_ok);
     TL_LAUNCH_CHECK();
     tl::count_launch();
   }

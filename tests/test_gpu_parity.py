@@ -579,3 +579,25 @@ def test_full_shape_store_vs_recompute_backward():
     assert torch.equal(a.report_tensor, b.report_tensor)
     assert _rel_fro(da, b.dhidden.float().cpu().numpy()) <= 5e-3
     assert _rel_fro(wa, b.dweight.cpu().numpy()) <= 5e-3
+
+
+def test_loss_fp32_unaligned_inputs():
+    """K3's 16-byte vector path needs aligned log-prob / grad / mask arrays;
+    views at odd offsets take the scalar path and give the same results."""
+    trajs, rewards, go, lnew, lold, lref = _synthetic_batch(3)
+    packed = packing.pack([_traj(s) for s in trajs])
+    T = packed.n_tokens
+
+    def view(a, off):
+        buf = torch.zeros(T + 4, dtype=torch.float32, device="cuda")
+        buf[off:off + T] = torch.from_numpy(a.astype(np.float32)).cuda()
+        return buf[off:off + T]
+
+    cfg = L.LossConfig(kl_beta=0.1)
+    ra, ga = grpo.grpo_loss(packed, go, rewards, view(lnew, 0), view(lold, 0), view(lref, 0), cfg)
+    rb, gb = grpo.grpo_loss(packed, go, rewards, view(lnew, 1), view(lold, 3), view(lref, 2), cfg)
+    for k in ("masked_tokens", "clamp_count", "clipped", "groups", "episodes"):
+        assert ra[k] == rb[k], k
+    for k in ("objective", "kl", "clip_fraction"):
+        assert abs(ra[k] - rb[k]) <= 1e-6 * max(1.0, abs(ra[k])), k
+    assert torch.equal(ga, gb)
