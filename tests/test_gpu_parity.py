@@ -601,3 +601,27 @@ def test_loss_fp32_unaligned_inputs():
     for k in ("objective", "kl", "clip_fraction"):
         assert abs(ra[k] - rb[k]) <= 1e-6 * max(1.0, abs(ra[k])), k
     assert torch.equal(ga, gb)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_step_with_no_action_tokens(mode):
+    """Edge case: every action segment empty (only observations carry
+    tokens).  The step must not touch the LM head: logp / entropy 0, dhidden
+    0, dweight 0, masked_tokens 0 and objective 0 (degenerate groups,
+    loss.py:173-174)."""
+    H, V = 128, 1000
+    trajs = [[("action", []), ("observation", [i % V, (i + 1) % V]), ("action", [])]
+             for i in range(8)]
+    packed = packing.pack([_traj(s) for s in trajs])
+    assert packed.n_act == 0 and packed.n_tokens == 16
+    g = torch.Generator(device="cuda").manual_seed(1)
+    h = torch.randn(packed.n_tokens, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.05).bfloat16()
+    lold = torch.zeros(packed.n_tokens, device="cuda")
+    go = np.array([0, 4, 8], dtype=np.int32)
+    res = grpo.GRPOStep(H, V, L.LossConfig(), **MODES[mode])(
+        packed, go, np.array([1.0, -1.0] * 4), h, W, lold)
+    torch.cuda.synchronize()
+    assert res.report["masked_tokens"] == 0 and res.report["objective"] == 0.0
+    assert not res.logp.any() and not res.entropy.any()
+    assert not res.dhidden.float().any() and not res.dweight.any()
