@@ -1,0 +1,330 @@
+// LM-head GEMM epilogues (included by lmhead.cu only; see its header for
+// the per-chunk pipeline):
+//   EpiLseStats   forward: per-row online log-sum-exp / E_p z / target logit
+//                 over a vocab strip, fp16 logit stores; the CTA finishing a
+//                 128-row block's last strip merges the strips and runs the
+//                 GRPO surrogate (combine_row).
+//   EpiDSoftmax   recompute mode: dS = dLoss/dz straight from TMEM.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "gemm_sm100.cuh"
+#include "grpo_token.cuh"
+
+namespace tl {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ------------------------------------------------------------- epilogues --
+__device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// 32 consecutive fp32 accumulator columns -> fp16 (saturating), 4 x 16-byte stores.
+// The stores carry an L2 eviction hint (`pol`): the chunk's logits are only
+// read back by the next kernel, so they should not push the wave's resident
+// h_c rows out of L2.
+__device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&r)[32], int nvalid,
+                                              uint64_t pol) {
+  if (nvalid >= 32) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 v;
+      v.x = pack_f16x2_sat(__uint_as_float(r[j + 0]), __uint_as_float(r[j + 1]));
+      v.y = pack_f16x2_sat(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      v.z = pack_f16x2_sat(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+      v.w = pack_f16x2_sat(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+      st_v4_hint(dst + j, v, pol);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)  // static indexing keeps r[] in registers
+      if (j < nvalid)
+        dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(__uint_as_float(r[j]), 0.f) & 0xFFFFu);
+  }
+}
+
+struct CombineArgs {
+  const float4* part;
+  int n_strips, rows;
+  const int32_t* idx;  // row -> packed position (nullable: identity)
+  // forward-only outputs (indexed by row)
+  float* logp_row;
+  float* ent_row;
+  float* lse_row;
+  // fused loss (nullable block: forward-only when logp_old == nullptr)
+  const int32_t* traj_of_token;
+  const float* logp_old;
+  const float* logp_ref;
+  const float* adv;
+  const float* traj_w;
+  tl_loss_config cfg;
+  float ent_grad;        // dLoss/dentropy per action token
+  float* logp_out;       // [T]
+  float* ent_out;        // [T]
+  float* term;           // [T]
+  float* k3o;            // [T]
+  uint8_t* flags;        // [T]
+  float* g_row;          // [C]
+  float* c_row;          // [C]
+  float* ez_row;         // [C]
+};
+
+// Merge a row's vocab-strip partials -> lse, logp, entropy; then the GRPO
+// surrogate on logp_new (grpo_token.cuh) -> per-token term / k3 / flags and
+// the row's dLoss/dlogp, dLoss/dent (K3 math fused into the log-prob
+// epilogue).  Partials written by other CTAs are read with ld.global.cg.
+__device__ void combine_row(const CombineArgs& a, int r) {
+  float m = -INFINITY, s = 0.f, t = 0.f, zy = -INFINITY;
+  for (int j = 0; j < a.n_strips; ++j) {
+    const float4 q = __ldcg(a.part + static_cast<long long>(j) * a.rows + r);
+    zy = fmaxf(zy, q.w);
+    if (q.x == -INFINITY) continue;
+    if (q.x > m) {
+      const float f = expf(m - q.x);
+      s = s * f + q.y;
+      t = t * f + q.z;
+      m = q.x;
+    } else {
+      const float f = expf(q.x - m);
+      s += q.y * f;
+      t += q.z * f;
+    }
+  }
+  const float lse = m + logf(s);
+  const float ez = t / s;
+  const float logp = zy - lse;
+  const float ent = lse - ez;
+  if (a.logp_row) a.logp_row[r] = logp;
+  if (a.ent_row) a.ent_row[r] = ent;
+  if (a.lse_row) a.lse_row[r] = lse;
+  if (a.logp_old) {
+    const long long p = a.idx ? a.idx[r] : r;
+    const int b = a.traj_of_token[p];
+    const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
+    const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
+    const float rf = a.cfg.has_ref ? a.logp_ref[p] : 0.f;
+    const TokTermF o = grpo_token_f32(logp, a.logp_old[p], rf, a.cfg.has_ref != 0 && rf == rf,
+                                      a.adv[b], lo, hi, static_cast<float>(a.cfg.kl_beta),
+                                      a.cfg.objective);
+    a.logp_out[p] = logp;
+    a.ent_out[p] = ent;
+    a.term[p] = o.term;
+    a.k3o[p] = o.k3;
+    a.flags[p] = o.flags;
+    a.g_row[r] = -o.dterm * a.traj_w[b];  // loss = -objective
+    a.c_row[r] = a.ent_grad;
+    a.ez_row[r] = ez;
+  }
+}
+
+// Online log-sum-exp over a vocab strip; one thread = one token row.
+struct EpiLseStats {
+  struct Params {
+    const int32_t* targets;  // [C] target id of each chunk row
+    float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
+    int rows;                // C (partials row stride)
+    __half_raw* zout;        // optional fp16 logit tile store [C, ldz] (backward input)
+    long long ldz;
+    int* tile_ctr;           // [ceil(C/128)] strips finished per 128-row block (zeroed)
+    CombineArgs ca;          // last-strip fixup: merge + surrogate for the block's rows
+    int z_policy;            // make_policy() kind of the fp16 logit stores
+  };
+  struct State {
+    float m, s, t, zy;
+    int y;
+    uint64_t zpol;
+  };
+  __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                    const UnitCoord&) {
+    st.m = -INFINITY;
+    st.s = 0.f;
+    st.t = 0.f;
+    st.zy = -INFINITY;
+    st.y = row < sh.M ? p.targets[row] : -1;
+    st.zpol = make_policy(p.z_policy);
+  }
+  // One 32-column slice of the row: fp16 store, running max rescale, then
+  // sum e and sum e*z with e = 2^(z*log2e - m*log2e).  Full slices (all but
+  // the vocab tail) take a branch-free path: 3-input max, one SFU op per
+  // logit, split accumulators; the target column is looked up only in the
+  // one slice that holds it.
+  __device__ static __forceinline__ void slice(const Params& p, const GemmShape& sh, State& st,
+                                               int row, int cb, const uint32_t (&r)[32]) {
+    const int nvalid = sh.N - cb;  // columns >= N are padding
+    if (p.zout && row < sh.M)
+      store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid, st.zpol);
+    const int yl = st.y - cb;
+    if (static_cast<unsigned>(yl) < 32u) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j == yl) st.zy = __uint_as_float(r[j]);
+    }
+    float cm;
+    if (nvalid >= 32) {
+      float m4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* v = reinterpret_cast<const float*>(r) + 8 * q;
+        m4[q] = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
+      }
+      cm = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+    } else {
+      cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) cm = fmaxf(cm, __uint_as_float(r[j]));
+    }
+    if (cm > st.m) {
+      const float f = ex2_ftz((st.m - cm) * kLog2e);
+      st.s *= f;
+      st.t *= f;
+      st.m = cm;
+    }
+    const float mb = st.m * kLog2e;
+    float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
+    if (nvalid >= 32) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+        const float e0 = ex2_ftz(fmaf(v0, kLog2e, -mb)), e1 = ex2_ftz(fmaf(v1, kLog2e, -mb));
+        s0 += e0;
+        s1 += e1;
+        t0 = fmaf(e0, v0, t0);
+        t1 = fmaf(e1, v1, t1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __uint_as_float(r[j]);
+        const float e = j < nvalid ? ex2_ftz(fmaf(v, kLog2e, -mb)) : 0.f;
+        s0 += e;
+        t0 = fmaf(e, v, t0);
+      }
+    }
+    st.s += s0 + s1;
+    st.t += t0 + t1;
+  }
+  // TMEM loads are double-buffered: slice c+1 is in flight while slice c is
+  // reduced (tcgen05.wait::ld waits for all outstanding loads).
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
+                              uint32_t taddr) {
+    static_assert(BN % 64 == 0, "slices are processed in pairs");
+    uint32_t ra[32], rb[32];
+    tmem_ld32(taddr, ra);
+    tmem_ld_wait_regs(ra);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 64) {
+      tmem_ld32(taddr + c + 32, rb);
+      slice(p, sh, st, row, col0 + c, ra);
+      tmem_ld_wait_regs(rb);
+      const bool more = c + 64 < BN;
+      if (more) tmem_ld32(taddr + c + 64, ra);
+      slice(p, sh, st, row, col0 + c + 32, rb);
+      if (more) tmem_ld_wait_regs(ra);
+    }
+  }
+  // Publish this strip's row stats; the CTA that finishes the LAST strip of a
+  // 128-row block (stream-K style fixup, counter per block) merges all strips
+  // and runs the GRPO surrogate for those rows inside this epilogue.
+  __device__ static void end_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                  const UnitCoord& uc) {
+    if (row < sh.M)
+      p.part[static_cast<long long>(uc.strip_idx) * p.rows + row] = make_float4(st.m, st.s, st.t, st.zy);
+    if (sh.n_strips == 1) {  // no other strip: merge straight away (own writes)
+      if (row < sh.M) combine_row(p.ca, row);
+      return;
+    }
+    __shared__ int s_last;
+    __threadfence();                                                   // release partials
+    asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");         // 4 epilogue warps
+    if ((threadIdx.x & 127) == 0) {
+      const int blk = row / kBM;
+      const int prev = atomicAdd(p.tile_ctr + blk, 1);
+      s_last = prev == sh.n_strips - 1;
+      if (s_last) p.tile_ctr[blk] = 0;  // re-arm for the next launch
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");
+    if (s_last) {
+      __threadfence();  // acquire the other strips' partials
+      if (row < sh.M) combine_row(p.ca, row);
+    }
+  }
+};
+
+// dS = dLoss/dz (bf16) from recomputed logits.
+struct EpiDSoftmax {
+  struct Params {
+    const int32_t* targets;
+    const float* lse;
+    const float* g;   // dLoss/dlogp
+    const float* c;   // dLoss/dentropy
+    const float* ez;  // E_p[z]
+    __nv_bfloat16_raw* ds;
+    long long ldd;
+  };
+  struct State {
+    float lse2, g, c, ez;
+    int y;
+  };
+  __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
+                                    const UnitCoord&) {
+    if (row < sh.M) {
+      st.lse2 = p.lse[row] * kLog2e;
+      st.g = p.g[row];
+      st.c = p.c[row];
+      st.ez = p.ez[row];
+      st.y = p.targets[row];
+    } else {
+      st.lse2 = 0.f;
+      st.g = st.c = st.ez = 0.f;
+      st.y = -1;
+    }
+  }
+  template <int BN>
+  __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
+                              uint32_t taddr) {
+    const bool row_ok = row < sh.M;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      const int cb = col0 + c;
+      float d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float z = __uint_as_float(r[j]);
+        const float pr = exp2f(fmaf(z, kLog2e, -st.lse2));
+        float v = -st.g * pr - st.c * pr * (z - st.ez);
+        if (cb + j == st.y) v += st.g;
+        d[j] = v;
+      }
+      __nv_bfloat16_raw* dst = p.ds + static_cast<long long>(row) * p.ldd + cb;
+      if (cb + 32 <= sh.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 v;
+          v.x = pack_bf16x2(d[j + 0], d[j + 1]);
+          v.y = pack_bf16x2(d[j + 2], d[j + 3]);
+          v.z = pack_bf16x2(d[j + 4], d[j + 5]);
+          v.w = pack_bf16x2(d[j + 6], d[j + 7]);
+          *reinterpret_cast<uint4*>(dst + j) = v;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (cb + j < sh.N) dst[j].x = static_cast<unsigned short>(pack_bf16x2(d[j], 0.f) & 0xFFFFu);
+      }
+    }
+  }
+  __device__ static void end_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+};
+
+}  // namespace
+}  // namespace tl
