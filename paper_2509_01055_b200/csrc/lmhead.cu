@@ -378,12 +378,12 @@ struct StreamPair {
 // is 2 strips x (n_pairs / 2) M-tiles, so the wave's h_c rows (37 x 256 x H
 // bf16 = 67 MB at C2) stay in L2 (evict_last) across the strip while every
 // W tile is fetched once per wave and shared by the n_pairs / 2 pairs of its
-// strip, kept close by the wave lockstep: sync steps of two tiles, window 1
-// (a producer may not start step s before every CTA of its strip group has
-// issued step s-1).  Measured at C2 (tools/experiments/gpu_r17, r25, r30):
+// strip, kept close by the wave lockstep: sync steps of eight tiles, window
+// 1 (a producer may not start step s before every CTA of its strip group has
+// issued step s-1).  Measured at C2 (tools/experiments/gpu_r17, r25, r30-r32):
 // one-tile window 2 -> 1 cut the forward's DRAM reads 33 -> 14 GB per chunk
 // (before serpentine K); per-strip instead of whole-wave groups -0.5 %;
-// two-tile steps -0.5 % (fewer waits, same DRAM).
+// 1 -> 2 -> 4 -> 8-tile steps -0.5 / -0.4 / -0.2 % (fewer waits).
 GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int n_tiles = (V + kBN - 1) / kBN;
   int strips = env_int("TL_FWD_STRIPS", kStripsFwd);
@@ -394,7 +394,7 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
                            env_int("TL_FWD_POLB", 0));
   // per-strip lockstep: a strip's 37 pairs (sharing its W tiles) wait on each
   // other only, not on the other strip of the wave
-  return with_sync(s, sync, 2 * s.k_blocks, 1, "FWD", 1);
+  return with_sync(s, sync, 8 * s.k_blocks, 1, "FWD", 1);
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
@@ -652,7 +652,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       // N-complete raster (group_m = 1): all H tiles of an M tile run together
       // so each dS k-block is fetched from HBM once; dS streams (evict first).
       const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
-                                     b.sync + 2 * kSyncWaves, 32, 1, "DH");
+                                     b.sync + 2 * kSyncWaves, 64, 1, "DH");
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
@@ -661,7 +661,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
     const GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
-                                   b.sync + 3 * kSyncWaves, 32, 1, "DW");
+                                   b.sync + 3 * kSyncWaves, 64, 1, "DW");
     EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };
