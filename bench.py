@@ -298,10 +298,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TL_BENCH_ONE_DEVICE=1 + TL_BENCH_BACKEND=gloo: every rank on cuda:0 over
+    # gloo — exercises the multi-rank path (sharding, N1/N2 all-reduces,
+    # max-over-ranks timing) on a one-GPU box with a small --config.
+    if os.environ.get("TL_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TL_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # global batch = world x config (weak scaling); whole groups per rank by LPT
     n_groups_global = cfg.prompts * world
