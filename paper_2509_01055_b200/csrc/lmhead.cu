@@ -359,7 +359,7 @@ struct StreamPair {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fwd = nullptr, ev_ds = nullptr;
   int err = TL_OK;
-  explicit StreamPair(cudaStream_t) {
+  StreamPair() {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo) != cudaSuccess ||
@@ -679,7 +679,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     //   main: F0 F1 . B0 F2 . B1 F3 . B2 ...      side: S0 (|| F1)  S1 (|| F2) ...
     // S_i is submitted after F_{i+1} so the GEMM's persistent CTAs are placed
     // first and the pass (a small grid-strided grid) fills the remaining slots.
-    StreamPair sp(st);
+    StreamPair sp;
     if (sp.err) return sp.err;
     const int ds_grid = env_int("TL_DS_OVERLAP_CTAS", 2) * num_sms();
     if (int e = stage_fwd(0)) return e;
