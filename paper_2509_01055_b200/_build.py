@@ -27,6 +27,7 @@ if os.environ.get("TL_GEMM_STATS") == "1":  # profiling build: GEMM stall counte
     FLAGS.append("-DTL_GEMM_STATS=1")
 if os.environ.get("TL_STAGES256"):  # tuning build: smem ring depth of 256-wide tiles
     FLAGS.append(f"-DTL_STAGES256={int(os.environ['TL_STAGES256'])}")
+FLAGS += os.environ.get("TL_EXTRA_NVCC_FLAGS", "").split()  # A/B builds on the GPU box
 
 
 def _headers() -> list[Path]:

@@ -439,6 +439,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ------------------------------------------------------- epilogue helpers --
+// Walk a thread's BN-wide accumulator row in 32-column slices, the next
+// slice's tcgen05.ld in flight while the current one is consumed by f(col,
+// regs) (the ld is warp-collective: every lane calls this, in-range or not).
+#ifndef TL_EPI_PIPELINE
+#define TL_EPI_PIPELINE 1
+#endif
+template <int BN, class F>
+__device__ __forceinline__ void tmem_row_slices(uint32_t taddr, F&& f) {
+  static_assert(BN % 64 == 0, "slices are processed in pairs");
+  if constexpr (!TL_EPI_PIPELINE) {  // A/B reference: one slice at a time
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait_regs(r);
+      f(c, r);
+    }
+    return;
+  }
+  uint32_t ra[32], rb[32];
+  tmem_ld32(taddr, ra);
+  tmem_ld_wait_regs(ra);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 64) {
+    tmem_ld32(taddr + c + 32, rb);
+    f(c, ra);
+    tmem_ld_wait_regs(rb);
+    const bool more = c + 64 < BN;
+    if (more) tmem_ld32(taddr + c + 64, ra);
+    f(c + 32, rb);
+    if (more) tmem_ld_wait_regs(ra);
+  }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -462,12 +496,8 @@ struct EpiStoreBF16 {
     const bool row_ok = row < s.M;
     long long orow = row;
     if (row_ok && p.row_map) orow = p.row_map[row];
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      if (!row_ok) continue;
+    tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
+      if (!row_ok) return;
       const int cb = col0 + c;
       __nv_bfloat16_raw* dst = p.out + orow * p.ldo + cb;
       if (cb + 32 <= s.N) {
@@ -489,7 +519,7 @@ struct EpiStoreBF16 {
           }
         }
       }
-    }
+    });
   }
 };
 
@@ -513,12 +543,8 @@ struct EpiStoreF32 {
   __device__ static void tile(const Params& p, const GemmShape& s, State&, int row, int col0,
                               uint32_t taddr) {
     const bool row_ok = row < s.M;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait();
-      if (!row_ok) continue;
+    tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
+      if (!row_ok) return;
       const int cb = col0 + c;
       float* dst = p.out + static_cast<long long>(row) * p.ldo + cb;
       if (cb + 32 <= s.N) {
@@ -543,7 +569,7 @@ struct EpiStoreF32 {
         for (int j = 0; j < 32; ++j)
           if (cb + j < s.N) dst[j] = (p.accumulate ? dst[j] : 0.f) + __uint_as_float(r[j]);
       }
-    }
+    });
   }
 };
 
