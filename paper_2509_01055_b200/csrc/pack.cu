@@ -120,6 +120,23 @@ __device__ __forceinline__ int find_segment(const int32_t* __restrict__ seg_dst,
   return lo - 1;
 }
 
+// Block-wide version of find_segment: every round each thread probes one of
+// blockDim.x evenly spaced segments of the current bracket; the probes with
+// seg_dst <= p form a prefix (seg_dst is non-decreasing), so its length
+// (__syncthreads_count) narrows the bracket blockDim.x-fold.
+__device__ __forceinline__ int block_find_segment(const int32_t* __restrict__ seg_dst, int n_seg,
+                                                  int p) {
+  int lo = 0, hi = n_seg;  // answer in [lo, hi); seg_dst[0] = 0 <= p
+  while (hi - lo > 1) {
+    const int step = (hi - lo + blockDim.x - 1) / blockDim.x;
+    const int idx = lo + static_cast<int>(threadIdx.x) * step;
+    const int cnt = __syncthreads_count(idx < hi && __ldg(seg_dst + idx) <= p);
+    lo += (cnt - 1) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 constexpr int kScatterThreads = 256;
 constexpr int kScatterRounds = 4;
 constexpr int kTilePos = kScatterThreads * 4 * kScatterRounds;  // packed positions per CTA
@@ -205,12 +222,13 @@ __global__ void __launch_bounds__(kScatterThreads)
   __shared__ int sh_range[2];
   const long long tile_begin = static_cast<long long>(blockIdx.x) * kTilePos;
   const long long tile_end = min(n_tokens, tile_begin + kTilePos);
-  if (threadIdx.x == 0) {
-    sh_range[0] = find_segment(seg_dst, n_seg, static_cast<int>(tile_begin));
-    sh_range[1] = find_segment(seg_dst, n_seg, static_cast<int>(tile_end - 1));
-  }
-  __syncthreads();
-  const int s_lo = sh_range[0], n_local = sh_range[1] - s_lo + 1;
+  // Segments holding the tile's first and last position: a block-wide
+  // 256-ary search (one probe per thread per round, 2 rounds up to 65 k
+  // segments) instead of one thread's 14 dependent loads.
+  const int s_first = block_find_segment(seg_dst, n_seg, static_cast<int>(tile_begin));
+  const int s_last = block_find_segment(seg_dst, n_seg, static_cast<int>(tile_end - 1));
+  (void)sh_range;
+  const int s_lo = s_first, n_local = s_last - s_lo + 1;
   if (n_local <= kSegCap) {
     for (int i = threadIdx.x; i < n_local; i += kScatterThreads) {
       const int s = s_lo + i;

@@ -1,7 +1,9 @@
 """Achieved HBM bandwidth of the memory-bound kernels at the C2 shape
 (north star: "achieved HBM GB/s for the packer, advantage and loss kernels
-against ~8 TB/s").  Each kernel is timed alone with CUDA events on the
-launching stream, L2 flushed (256 MB write) before every timed launch;
+against ~8 TB/s").  Each operation is timed alone, L2 flushed (256 MB
+write) before every timed launch, two ways: CUDA events around the public
+Python call (includes host work and allocations) and, for the rows marked
+"device", the library's own events around its kernel launches;
 GB/s = algorithmic bytes / median time.  Prints one JSON line."""
 
 import json
@@ -37,6 +39,22 @@ def timed(fn, iters=None):
     return float(np.median(ts[2:]))
 
 
+def device_ms(fn, cat, iters=5):
+    """Median device time of the kernels `fn` launches in profile category
+    `cat` (CUDA events recorded by the library around its own launches, so
+    host / Python / allocation time is excluded); L2 flushed before each."""
+    ts = []
+    for _ in range(iters):
+        FLUSH.fill_(1)
+        torch.cuda.synchronize()
+        _lib.profile_enable(True)
+        fn()
+        torch.cuda.synchronize()
+        ts.append(_lib.profile_read()[cat][0])
+        _lib.profile_enable(False)
+    return float(np.median(ts))
+
+
 def main():
     cfg = CONFIGS["c2"]
     wl = make_workload(cfg)
@@ -53,6 +71,8 @@ def main():
     # read ids 4 + write ids 4, mask 1, positions 4, traj 4 per token; act_idx 4 per action token
     by = 21 * T + 4 * A + 13 * S + 8 * (B + 1)
     res["pack_varlen (K1)"] = (ms, by)
+    res["pack_varlen (K1) device"] = (device_ms(
+        lambda: packing.pack_table(tab, device=dev, validate=False, device_inputs=dtab), "pack"), by)
 
     lmax = int((packed.cu_seqlens[1:] - packed.cu_seqlens[:-1]).max())
     ms = timed(lambda: packing.pad(packed, lmax=lmax))
@@ -70,6 +90,8 @@ def main():
     ms = timed(lambda: grpo.grpo_loss(packed, go, rw, lnew, lold, lref, c))
     # mask 1 B/token, logp_new/old/ref 12 B per action token, grad 4 B/token
     res["grpo_loss fp32 (K3, incl. K2 + report)"] = (ms, 5 * T + 12 * A)
+    res["grpo_loss fp32 (K3 + group/report reductions) device"] = (device_ms(
+        lambda: grpo.grpo_loss(packed, go, rw, lnew, lold, lref, c), "loss"), 5 * T + 12 * A)
 
     # dsoftmax on one chunk and the row gather, via the fused step's profile
     H, V = cfg.hidden, cfg.vocab
