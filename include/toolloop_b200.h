@@ -12,6 +12,9 @@
  * (MaskMismatch, GroupTooSmall, ValueError) is done by the host caller on
  * host-side metadata before launch; the codes below carry the same meaning.
  *
+ * The F1 ingest (tl_ingest_*) and F4 tokeniser (tl_tokenizer_*,
+ * tl_tokenize_segments) entry points are host-only: host pointers, no stream.
+ *
  * Data types: token ids int32, masks uint8, bf16 tensors as uint16_t bit
  * patterns, log-probs float (perf mode) or double (parity mode).
  */
