@@ -365,7 +365,8 @@ MODES = {"store": {}, "recompute": {"recompute": True}, "pipelined": {"pipelined
 
 
 @pytest.mark.parametrize("mode", list(MODES))
-@pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256), (192, 517, 128)])
+@pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256), (192, 517, 128),
+                                       (128, 1000, 200)])
 def test_grpo_lmhead_step_vs_oracle(H, V, chunk, mode):
     from oracle import lmhead_oracle as LH
 
