@@ -4,8 +4,8 @@
 // TMEM.  Both operands may be K-major or MN-major in global memory; TMA
 // (SWIZZLE_128B) stages them into a STAGES-deep shared-memory ring, one
 // elected thread issues tcgen05.mma (K=16), accumulators are double-buffered
-// in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of
-// tile i+1.
+// in TMEM (2 x BN columns, BN <= 256) so the epilogue of tile i overlaps the
+// MMAs of tile i+1; BN = 512 tiles (dH / dW) use all 512 columns once.
 //
 // CG = 1: one CTA per tile, UMMA 128 x BN.
 // CG = 2: a 2-CTA cluster (one TPC) per tile, UMMA 256 x BN issued by the
@@ -29,6 +29,16 @@
 // units share A and B tiles in L2; unit u runs on CTA(-pair) u % n_pairs.  The
 // epilogue sees begin_unit / tile / end_unit so row-wise reductions over a
 // strip (the online log-sum-exp of the LM head) stay in registers.
+//
+// L2 reuse across CTAs (the step is energy-bound):
+//   wave lockstep  the i-th units of all CTA pairs form wave i; producers
+//                  publish progress on a per-wave (or per-(wave, strip)
+//                  group) counter and may run at most `sync_window` sync
+//                  steps ahead of the slowest member, so tiles that share an
+//                  operand load it while it is still in L2;
+//   serpentine K   tiles of odd (wave + tile) parity stream their k-blocks
+//                  last-to-first, starting on what the previous tile (and
+//                  the wave) read last.
 #pragma once
 #include <cuda_bf16.h>
 
