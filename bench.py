@@ -470,7 +470,8 @@ def main():
 
     peak_s, peak_b, hbm, peak_kind = _peaks()
     flops_alg = 6.0 * n_act * H * V      # fwd logp (2) + dH (2) + dW (2), action rows only
-    flops_issued = 8.0 * n_act * H * V   # + logits recompute in the backward
+    # issued tensor FLOPs: the recompute mode runs the logits GEMM a second time
+    flops_issued = (8.0 if args.mode == "recompute" else 6.0) * n_act * H * V
     gemm_ms = sum(prof.get(k, (0, 0))[0] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     gemm_launch = sum(prof.get(k, (0, 0))[1] for k in ("gemm_fwd", "gemm_dsoftmax", "gemm_dh", "gemm_dw"))
     roofline = None
