@@ -107,6 +107,17 @@ struct GemmShape {
   // last — still in L2 when the operand is too large to stay resident.  Only
   // the producer's block order changes (fixed per tile: deterministic).
   int serpentine;
+  // Split-K tail (strip == 1 shapes, epilogues with Epi::kSplitTail; set by
+  // the launcher once it knows the number of co-resident pairs): the units of
+  // a partial last wave [tail_begin, n_units) are cut into tail_split
+  // K-slices that run as separate work items on the otherwise idle pairs.
+  // Each slice writes its fp32 partial tile to tail_part; the slice that
+  // arrives last for a tile half (counter tail_ctr) sums all slices in slice
+  // order and hands the sum to the epilogue's final write: deterministic.
+  int tail_begin;    // == n_units: off
+  int tail_split;
+  float* tail_part;  // [(n_units - tail_begin) * tail_split][cg][kBM][BN]
+  int* tail_ctr;     // [(n_units - tail_begin) * cg], zeroed before launch
 };
 
 struct UnitCoord {
@@ -136,6 +147,35 @@ __host__ __device__ inline UnitCoord unit_coord(const GemmShape& s, int u) {
   return c;
 }
 
+// Work item i of the persistent schedule: a whole unit, or (tail) one
+// K-slice [kb_begin, kb_end) of a unit; piece = slice index among all tail
+// slices, -1 for a whole unit.
+struct WorkItem {
+  int unit, kb_begin, kb_end, piece;
+};
+
+__host__ __device__ inline int n_work_items(const GemmShape& s) {
+  return s.tail_begin + (s.n_units - s.tail_begin) * s.tail_split;
+}
+
+__host__ __device__ inline WorkItem work_item(const GemmShape& s, int i) {
+  WorkItem w;
+  if (i < s.tail_begin) {
+    w.unit = i;
+    w.kb_begin = 0;
+    w.kb_end = s.k_blocks;
+    w.piece = -1;
+    return w;
+  }
+  const int q = i - s.tail_begin;
+  const int t = q / s.tail_split, sl = q - t * s.tail_split;
+  w.unit = s.tail_begin + t;
+  w.kb_begin = static_cast<int>(static_cast<long long>(s.k_blocks) * sl / s.tail_split);
+  w.kb_end = static_cast<int>(static_cast<long long>(s.k_blocks) * (sl + 1) / s.tail_split);
+  w.piece = q;
+  return w;
+}
+
 inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m, int cg = 1,
                             int pol_a = 0, int pol_b = 0) {
   GemmShape s;
@@ -150,6 +190,9 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m,
   s.sync_window = 0;
   s.sync_split = 0;
   s.serpentine = 0;
+  s.tail_split = 1;
+  s.tail_part = nullptr;
+  s.tail_ctr = nullptr;
   s.m_tiles = (M + kBM * cg - 1) / (kBM * cg);
   s.n_tiles = (N + BN - 1) / BN;
   s.k_blocks = (K + kBK - 1) / kBK;
@@ -157,6 +200,7 @@ inline GemmShape make_shape(int M, int N, int K, int BN, int strip, int group_m,
   s.n_strips = (s.n_tiles + s.strip - 1) / s.strip;
   s.group_m = group_m < 1 ? 1 : (group_m > s.m_tiles ? s.m_tiles : group_m);
   s.n_units = s.m_tiles * s.n_strips;
+  s.tail_begin = s.n_units;
   return s;
 }
 
@@ -177,6 +221,40 @@ struct GemmSmem {
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
   static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1 KB align
 };
+
+// Walk a thread's BN-wide accumulator row in 32-column slices, the next
+// slice's tcgen05.ld in flight while the current one is consumed by f(col,
+// regs) (the ld is warp-collective: every lane calls this, in-range or not).
+#ifndef TL_EPI_PIPELINE
+#define TL_EPI_PIPELINE 1
+#endif
+template <int BN, class F>
+__device__ __forceinline__ void tmem_row_slices(uint32_t taddr, F&& f) {
+  static_assert(BN % 64 == 0, "slices are processed in pairs");
+  if constexpr (!TL_EPI_PIPELINE) {  // A/B reference: one slice at a time
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c, r);
+      tmem_ld_wait_regs(r);
+      f(c, r);
+    }
+    return;
+  }
+  uint32_t ra[32], rb[32];
+  tmem_ld32(taddr, ra);
+  tmem_ld_wait_regs(ra);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 64) {
+    tmem_ld32(taddr + c + 32, rb);
+    f(c, ra);
+    tmem_ld_wait_regs(rb);
+    const bool more = c + 64 < BN;
+    if (more) tmem_ld32(taddr + c + 64, ra);
+    f(c + 32, rb);
+    if (more) tmem_ld_wait_regs(ra);
+  }
+}
 
 template <int BN, int STAGES, int CG, bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -240,20 +318,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int wave = 0;
-      for (int u = pair; u < shape.n_units; u += n_pairs, ++wave) {
+      const int n_items = n_work_items(shape);
+      for (int it = pair; it < n_items; it += n_pairs, ++wave) {
+        const WorkItem wi = work_item(shape, it);
+        const int u = wi.unit;
+        const int nkb = wi.kb_end - wi.kb_begin;
         const UnitCoord uc = unit_coord(shape, u);
         const int m0 = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM;
         int* ctr = nullptr;
         int wave_ctas = 0;
         if (shape.sync_ctr) {
           const int w0 = wave * n_pairs;
-          const int wn = min(n_pairs, shape.n_units - w0);
+          const int wn = min(n_pairs, n_items - w0);
           if (shape.sync_split) {
-            auto key = [&](int uu) {
-              const UnitCoord c = unit_coord(shape, uu);
+            auto key = [&](int ii) {
+              const UnitCoord c = unit_coord(shape, work_item(shape, ii).unit);
               return (c.m_tile / shape.group_m) * shape.n_strips + c.strip_idx;
             };
-            const int km = key(u);
+            const int km = key(it);
             int cnt = 0;
             for (int j = 0; j < wn; ++j) cnt += key(w0 + j) == km;
             const int slot = km - key(w0);  // keys ascend within a wave
@@ -272,7 +354,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // stages rows rank*kBRows.. of each (the pair MMA splits B in half)
           const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
           const bool rev = shape.serpentine && ((wave + t) & 1);
-          for (int kb = 0; kb < shape.k_blocks; ++kb) {
+          for (int kb = 0; kb < nkb; ++kb) {
             if (ctr && do_wait && in_step == 0 && sstep >= shape.sync_window) {
               // The lockstep only shapes L2 reuse, never correctness: a wait that
               // exceeds ~50 ms (co-residency lost, preemption) stops waiting for
@@ -298,7 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint8_t* sa = smem + stage * Smem::kStageBytes;
             uint8_t* sb = sa + Smem::kABytes;
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], CG * Smem::kStageBytes);
-            const int k0 = (rev ? shape.k_blocks - 1 - kb : kb) * kBK;
+            const int k0 = (rev ? wi.kb_end - 1 - kb : wi.kb_begin + kb) * kBK;
             auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1, uint64_t pol) {
               if constexpr (CG == 2) tma_load_2d_cg2(m, &full_bar[stage], dst, c0, c1, pol);
               else tma_load_2d(m, &full_bar[stage], dst, c0, c1, pol);
@@ -348,8 +430,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       TL_STAT_BEGIN(t_all);
-      for (int u = pair; u < shape.n_units; u += n_pairs) {
-        const UnitCoord uc = unit_coord(shape, u);
+      const int n_items = n_work_items(shape);
+      for (int it = pair; it < n_items; it += n_pairs) {
+        const WorkItem wi = work_item(shape, it);
+        const int nkb = wi.kb_end - wi.kb_begin;
+        const UnitCoord uc = unit_coord(shape, wi.unit);
         for (int t = 0; t < uc.n_count; ++t) {
           {
             TL_STAT_BEGIN(t_te);
@@ -358,7 +443,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * BN;
-          for (int kb = 0; kb < shape.k_blocks; ++kb) {
+          for (int kb = 0; kb < nkb; ++kb) {
             {
               TL_STAT_BEGIN(t_f);
               mbar_wait(&full_bar[stage], phase);
@@ -405,8 +490,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     typename Epi::State st;
-    for (int u = pair; u < shape.n_units; u += n_pairs) {
-      const UnitCoord uc = unit_coord(shape, u);
+    const int n_items = n_work_items(shape);
+    for (int it = pair; it < n_items; it += n_pairs) {
+      const WorkItem wi = work_item(shape, it);
+      const UnitCoord uc = unit_coord(shape, wi.unit);
       const int row = uc.m_tile * kBM * CG + static_cast<int>(rank) * kBM + row_in_tile;
       Epi::begin_unit(ep, shape, st, row, uc);
       for (int t = 0; t < uc.n_count; ++t) {
@@ -418,7 +505,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
         TL_STAT_BEGIN(t_tile);
-        Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
+        if constexpr (Epi::kSplitTail) {
+          if (wi.piece >= 0) {
+            // tail slice: park this slice's fp32 partial tile (this CTA's rows)
+            float* part = shape.tail_part +
+                          ((static_cast<long long>(wi.piece) * CG + rank) * kBM + row_in_tile) * BN;
+            tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                __stcg(reinterpret_cast<float4*>(part + c + j),
+                       make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+            });
+          } else {
+            Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
+          }
+        } else {
+          Epi::template tile<BN>(ep, shape, st, row, (uc.n_begin + t) * BN, taddr);
+        }
         if (lane == 0 && q == 0) TL_STAT_END(t_tile, ST_EPI_TILE);
         tc_fence_before();
         __syncwarp();
@@ -432,7 +536,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       TL_STAT_BEGIN(t_end);
-      Epi::end_unit(ep, shape, st, row, uc);
+      if constexpr (Epi::kSplitTail) {
+        if (wi.piece >= 0) {
+          // the last slice to arrive for this tile half sums all slices in
+          // slice order (deterministic) and performs the epilogue's write
+          __shared__ int s_last;
+          __threadfence();                                            // release the partial
+          asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");  // 4 epilogue warps
+          const int t_local = wi.unit - shape.tail_begin;
+          if (q == 0 && lane == 0) {
+            int* c = shape.tail_ctr + t_local * CG + rank;
+            const int prev = atomicAdd(c, 1);
+            s_last = prev == shape.tail_split - 1;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(4 * 32) : "memory");
+          if (s_last) {
+            __threadfence();  // acquire the other slices' partials
+            const float* p0 = shape.tail_part +
+                              ((static_cast<long long>(t_local) * shape.tail_split * CG + rank) * kBM +
+                               row_in_tile) * BN;
+            const long long slice_stride = static_cast<long long>(CG) * kBM * BN;
+            for (int c = 0; c < BN; c += 4) {
+              float4 v = __ldcg(reinterpret_cast<const float4*>(p0 + c));
+              for (int sl = 1; sl < shape.tail_split; ++sl) {
+                const float4 w = __ldcg(reinterpret_cast<const float4*>(p0 + sl * slice_stride + c));
+                v.x += w.x;
+                v.y += w.y;
+                v.z += w.z;
+                v.w += w.w;
+              }
+              Epi::store4(ep, shape, row, uc.n_begin * BN + c, v);
+            }
+          }
+        } else {
+          Epi::end_unit(ep, shape, st, row, uc);
+        }
+      } else {
+        Epi::end_unit(ep, shape, st, row, uc);
+      }
       if (lane == 0 && q == 0) TL_STAT_END(t_end, ST_EPI_END);
     }
   }
@@ -449,40 +590,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ------------------------------------------------------- epilogue helpers --
-// Walk a thread's BN-wide accumulator row in 32-column slices, the next
-// slice's tcgen05.ld in flight while the current one is consumed by f(col,
-// regs) (the ld is warp-collective: every lane calls this, in-range or not).
-#ifndef TL_EPI_PIPELINE
-#define TL_EPI_PIPELINE 1
-#endif
-template <int BN, class F>
-__device__ __forceinline__ void tmem_row_slices(uint32_t taddr, F&& f) {
-  static_assert(BN % 64 == 0, "slices are processed in pairs");
-  if constexpr (!TL_EPI_PIPELINE) {  // A/B reference: one slice at a time
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(taddr + c, r);
-      tmem_ld_wait_regs(r);
-      f(c, r);
-    }
-    return;
-  }
-  uint32_t ra[32], rb[32];
-  tmem_ld32(taddr, ra);
-  tmem_ld_wait_regs(ra);
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 64) {
-    tmem_ld32(taddr + c + 32, rb);
-    f(c, ra);
-    tmem_ld_wait_regs(rb);
-    const bool more = c + 64 < BN;
-    if (more) tmem_ld32(taddr + c + 64, ra);
-    f(c + 32, rb);
-    if (more) tmem_ld_wait_regs(ra);
-  }
-}
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -492,6 +599,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // Plain store of the fp32 accumulator as bf16 (optionally with a row remap),
 // used for the dH GEMM (rows scattered back to packed positions) and tests.
 struct EpiStoreBF16 {
+  static constexpr bool kSplitTail = false;
   struct Params {
     __nv_bfloat16_raw* out;
     long long ldo;          // elements
@@ -540,6 +648,7 @@ struct EpiStoreBF16 {
 // would stall the next tile's MMAs.  Each element has one writer per launch,
 // so both forms give the same bits.
 struct EpiStoreF32 {
+  static constexpr bool kSplitTail = true;
   struct Params {
     float* out;
     long long ldo;
@@ -549,36 +658,39 @@ struct EpiStoreF32 {
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
   __device__ static void end_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
+  // out[row, col .. col+3] (+)= v  (also the final write of a split-K tail tile)
+  __device__ static __forceinline__ void store4(const Params& p, const GemmShape& s, int row,
+                                                int col, float4 v) {
+    if (row >= s.M) return;
+    float* dst = p.out + static_cast<long long>(row) * p.ldo + col;
+    if (col + 4 <= s.N) {
+      if (p.accumulate && !p.load_add) {
+        red_add_v4_f32(dst, v);
+        return;
+      }
+      if (p.accumulate) {
+        const float4 o = *reinterpret_cast<const float4*>(dst);
+        v.x += o.x;
+        v.y += o.y;
+        v.z += o.z;
+        v.w += o.w;
+      }
+      *reinterpret_cast<float4*>(dst) = v;
+    } else {
+      const float e[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < 4; ++j)
+        if (col + j < s.N) dst[j] = (p.accumulate ? dst[j] : 0.f) + e[j];
+    }
+  }
   template <int BN>
   __device__ static void tile(const Params& p, const GemmShape& s, State&, int row, int col0,
                               uint32_t taddr) {
-    const bool row_ok = row < s.M;
     tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
-      if (!row_ok) return;
-      const int cb = col0 + c;
-      float* dst = p.out + static_cast<long long>(row) * p.ldo + cb;
-      if (cb + 32 <= s.N) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                 __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-          if (p.accumulate && !p.load_add) {
-            red_add_v4_f32(dst + j, v);
-            continue;
-          }
-          if (p.accumulate) {
-            const float4 o = *reinterpret_cast<const float4*>(dst + j);
-            v.x += o.x;
-            v.y += o.y;
-            v.z += o.z;
-            v.w += o.w;
-          }
-          *reinterpret_cast<float4*>(dst + j) = v;
-        }
-      } else {
-        for (int j = 0; j < 32; ++j)
-          if (cb + j < s.N) dst[j] = (p.accumulate ? dst[j] : 0.f) + __uint_as_float(r[j]);
-      }
+      for (int j = 0; j < 32; j += 4)
+        store4(p, s, row, col0 + c + j,
+               make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                           __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
     });
   }
 };

@@ -111,6 +111,9 @@ int make_ab_maps(CUtensorMap* ma, CUtensorMap* mb, const void* A, bool a_mn, lon
 unsigned long long* h_stats_base = nullptr;  // [PROF categories][160 CTAs][8]
 #endif
 
+// split-K tail slice buffer: tile halves of 128 rows x 512 fp32 columns
+constexpr int kTailSlots = 160;
+
 template <int CG, bool A_MN, bool B_MN, class Epi, int BN = kBN>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
                 const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
@@ -147,13 +150,29 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
   const int groups = s.n_units < max_groups ? s.n_units : max_groups;
   lc.gridDim = dim3(groups * CG);
+  GemmShape sh = s;
+  if constexpr (Epi::kSplitTail) {
+    // split-K tail: cut the partial last wave's units into K-slices that fill
+    // the idle pairs (slice buffer holds one wave: kTailSlots tile halves)
+    const int rem = sh.n_units % groups;
+    if (sh.tail_part && sh.strip == 1 && rem > 0 && sh.n_units > groups) {
+      int split = groups / rem;
+      split = split < sh.k_blocks ? split : sh.k_blocks;
+      if (rem * split * CG > kTailSlots) split = kTailSlots / (rem * CG);
+      if (split >= 2) {
+        sh.tail_begin = sh.n_units - rem;
+        sh.tail_split = split;
+        TL_CUDA_TRY(cudaMemsetAsync(sh.tail_ctr, 0, rem * CG * sizeof(int), st));
+      }
+    }
+  }
 #if TL_GEMM_STATS
   if (h_stats_base) {  // stream-ordered: this launch's counters go to its category's block
     unsigned long long* p = h_stats_base + static_cast<size_t>(prof_cat) * 160 * 8;
     TL_CUDA_TRY(cudaMemcpyToSymbolAsync(g_gemm_stats, &p, sizeof(p), 0, cudaMemcpyHostToDevice, st));
   }
 #endif
-  TL_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, s, ep));
+  TL_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, sh, ep));
   count_launch();
   return TL_OK;
 }
@@ -280,6 +299,8 @@ struct ChunkWs {
   double* traj_out; // [B*8]
   double* group_out;// [G*8]
   int* sync;        // [3 * kSyncWaves] wave-lockstep counters (fwd / dH / dW)
+  float* tail_part; // [kTailSlots][128][512] split-K tail slices of the dW GEMM
+  int* tail_ctr;    // [kTailSlots] slice arrival counters
 };
 
 constexpr int kSyncWaves = 4096;
@@ -331,6 +352,10 @@ void carve_chunk(Workspace& w, ChunkWs& c, int C, int H, int V, bool with_bwd) {
   c.ent = w.take<float>(C);
   c.ds = with_bwd ? w.take<uint16_t>(static_cast<size_t>(C) * vld_of(V)) : nullptr;
   c.sync = w.take<int>(5 * kSyncWaves);
+  if (with_bwd) {
+    c.tail_part = w.take<float>(static_cast<size_t>(kTailSlots) * kBM * kBNWide);
+    c.tail_ctr = w.take<int>(kTailSlots);
+  }
 }
 
 ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool with_bwd,
@@ -660,8 +685,12 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     }
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
-    const GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
-                                   b.sync + 3 * kSyncWaves, 64, 1, "DW");
+    GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
+                             b.sync + 3 * kSyncWaves, 64, 1, "DW");
+    if (env_int("TL_DW_TAIL", 1)) {  // split-K tail for the partial last wave
+      sh.tail_part = b.tail_part;
+      sh.tail_ctr = b.tail_ctr;
+    }
     EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };

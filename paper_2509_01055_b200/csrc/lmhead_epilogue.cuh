@@ -124,6 +124,7 @@ __device__ void combine_row(const CombineArgs& a, int r) {
 
 // Online log-sum-exp over a vocab strip; one thread = one token row.
 struct EpiLseStats {
+  static constexpr bool kSplitTail = false;
   struct Params {
     const int32_t* targets;  // [C] target id of each chunk row
     float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
@@ -259,6 +260,7 @@ struct EpiLseStats {
 
 // dS = dLoss/dz (bf16) from recomputed logits.
 struct EpiDSoftmax {
+  static constexpr bool kSplitTail = false;
   struct Params {
     const int32_t* targets;
     const float* lse;

@@ -626,3 +626,60 @@ def test_step_with_no_action_tokens(mode):
     assert res.report["masked_tokens"] == 0 and res.report["objective"] == 0.0
     assert not res.logp.any() and not res.entropy.any()
     assert not res.dhidden.float().any() and not res.dweight.any()
+
+
+def test_dw_split_k_tail_vs_oracle():
+    """dW GEMM with a partial last wave (V 3072 = 12 vocab tiles x 7 hidden
+    tiles = 84 units on 74 pairs): the 10 tail units run as K-slices on the
+    idle pairs and the last slice to arrive sums them in order.  Checked
+    against the oracle backward across several chunks (store and accumulate
+    epilogues), bitwise run to run, and against the unsplit kernel."""
+    import os
+
+    from oracle import lmhead_oracle as LH
+
+    H, V = 3584, 3072
+    trajs, rewards, go, _, lold, lref = _synthetic_batch(12, n_groups=6, G=4)
+    for tr in trajs:
+        for i, (o, toks) in enumerate(tr):
+            tr[i] = (o, [t % V for t in toks])
+    packed = packing.pack([_traj(s) for s in trajs])
+    T = packed.n_tokens
+    g = torch.Generator(device="cuda").manual_seed(31)
+    h = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, H, device="cuda", generator=g) * 0.02).bfloat16()
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()  # noqa: E731
+    cfg = L.LossConfig(kl_beta=0.1, entropy_coef=0.01)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=512)
+    assert packed.n_act > 1024  # several chunks
+    r1 = step(packed, go, rewards, h, W, f(lold), f(lref))
+    dw1 = r1.dweight.clone()
+    r2 = step(packed, go, rewards, h, W, f(lold), f(lref))
+    assert torch.equal(dw1, r2.dweight)
+    os.environ["TL_DW_TAIL"] = "0"
+    try:
+        r3 = step(packed, go, rewards, h, W, f(lold), f(lref))
+    finally:
+        del os.environ["TL_DW_TAIL"]
+    assert _rel_fro(dw1.cpu().numpy(), r3.dweight.cpu().numpy()) <= 1e-6
+    # oracle
+    ids = packed.input_ids.cpu().numpy()
+    act = packed.act_idx.cpu().numpy()
+    hn, Wn = _bf16_np(h), _bf16_np(W)
+    lp, _, _ = LH.lmhead_forward(hn[act], Wn, ids[act], exact=True)
+    lnew = np.zeros(T)
+    lnew[act] = lp
+    lo32 = lold.astype(np.float32).astype(np.float64)
+    lr32 = lref.astype(np.float32).astype(np.float64)
+    _, groups = _oracle_report(trajs, rewards, go, lnew, lo32, lr32, beta=0.1)
+    n_groups = len(go) - 1
+    gl = np.zeros(T)
+    pos = 0
+    for recs_g, rw in groups:
+        for row in O.clipped_grad(recs_g, O.group_advantages(rw), 0.2, 0.1):
+            for e in row:
+                gl[pos] = -e / n_groups
+                pos += 1
+    cg = np.full(len(act), -0.01 / len(act))
+    _, dW = LH.lmhead_backward(hn[act], Wn, ids[act], gl[act], cg)
+    assert _rel_fro(dw1.cpu().numpy(), dW) <= 2e-2
