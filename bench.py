@@ -507,7 +507,7 @@ def main():
                    "tokens_per_step": int(T_all), "action_tokens_per_step": int(A_all),
                    "action_tokens_per_s": A_all / (ms / 1e3),
                    "parallelism": f"dp{world} (groups, LPT)", "l2": "inputs >> L2 (hidden is GBs)",
-                   "chunk_rows": step._chunk(max(w.n_act for w in wls)), "loss_agg": cfg.loss_agg,
+                   "chunk_rows": step.last_chunk, "loss_agg": cfg.loss_agg,
                    "micro_batches": len(mbs),
                    "lmhead_mode": args.mode},
         "roofline": roofline,

@@ -29,6 +29,11 @@ REPORT_KEYS = ("objective", "clip_fraction", "masked_tokens", "kl", "groups", "e
                "objective_sum")
 
 DEFAULT_CHUNK_ROWS = 148 * 128 * 2  # two 128-row M-tiles per SM per vocab strip wave
+# The step picks the largest multiple (up to this) of DEFAULT_CHUNK_ROWS
+# whose workspace fits in half of the free HBM: fewer, larger chunks amortise
+# each GEMM's ramp / tail and the dW accumulation (C2: 2x -0.7 %, 4x -1.2 %,
+# tools/experiments/gpu_r43.sh).  Pass chunk_rows for a fixed size.
+MAX_CHUNK_MULT = 4
 
 
 def report_dict(rep) -> dict:
@@ -129,16 +134,34 @@ class GRPOStep:
         else:
             self.mode = _lib.LMHEAD_STORE_LOGITS
         self._ws = _Workspace()
+        self.last_chunk = None  # chunk rows used by the latest call
 
     def workspace_bytes(self, n_act: int, n_tokens: int, n_traj: int, n_groups: int) -> int:
         L = _lib.lib()
         return int(L.tl_lmhead_step_workspace_bytes(self._chunk(n_act), self.H, self.V, n_tokens,
                                                     n_traj, n_groups, self.mode))
 
-    def _chunk(self, n_act: int) -> int:
+    def _chunk(self, n_act: int, n_tokens: int = 0, n_traj: int = 0, n_groups: int = 0,
+               device=None) -> int:
         if self.chunk_rows:
             return int(self.chunk_rows)
-        return int(min(DEFAULT_CHUNK_ROWS, max(128, (n_act + 127) // 128 * 128)))
+        rows = max(128, (n_act + 127) // 128 * 128)
+        if rows <= DEFAULT_CHUNK_ROWS:
+            return int(rows)
+        mult = min(MAX_CHUNK_MULT, -(-n_act // DEFAULT_CHUNK_ROWS))
+        if device is not None and mult > 1:
+            import torch
+
+            L = _lib.lib()
+            free, _ = torch.cuda.mem_get_info(device)
+            free += torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+            if self._ws.buf is not None and self._ws.buf.device == device:
+                free += self._ws.buf.numel()
+            while mult > 1 and L.tl_lmhead_step_workspace_bytes(
+                    mult * DEFAULT_CHUNK_ROWS, self.H, self.V, n_tokens, n_traj, n_groups,
+                    self.mode) > free // 2:
+                mult -= 1
+        return int(mult * DEFAULT_CHUNK_ROWS)
 
     def __call__(self, packed: PackedBatch, group_off, rewards, hidden, weight, logp_old,
                  logp_ref=None, *, backward: bool = True, norm_groups: float | None = None,
@@ -193,7 +216,8 @@ class GRPOStep:
         rep = out.get("report")
         if rep is None:
             rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
-        chunk = self._chunk(packed.n_act)
+        chunk = self._chunk(packed.n_act, T, packed.n_traj, n_groups, dev)
+        self.last_chunk = chunk
         ws_bytes = int(L.tl_lmhead_step_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
                                                         n_groups, self.mode))
         ws = self._ws.get(ws_bytes, dev)
