@@ -306,7 +306,8 @@ def lmhead_logprobs(hidden, weight, targets, rows=None, *, chunk_rows: int | Non
     V = weight.shape[0]
     n = hidden.shape[0] if rows is None else rows.shape[0]
     dev = hidden.device
-    chunk = int(chunk_rows or min(DEFAULT_CHUNK_ROWS, max(128, (n + 127) // 128 * 128)))
+    # forward-only workspace is small (h_c + per-row stats): always the largest chunk
+    chunk = int(chunk_rows or min(MAX_CHUNK_MULT * DEFAULT_CHUNK_ROWS, max(128, (n + 127) // 128 * 128)))
     ws_bytes = int(L.tl_lmhead_workspace_bytes(chunk, H, V, 0, 0, 0))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     logp = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
