@@ -547,7 +547,7 @@ def test_lmhead_full_shape_sampled_rows():
     h = torch.randn(n, H, device="cuda", generator=g).bfloat16()
     W = (torch.randn(V, H, device="cuda", generator=g) * 0.02).bfloat16()
     y = torch.randint(0, V, (n,), device="cuda", generator=g, dtype=torch.int32)
-    logp, ent, lse = grpo.lmhead_logprobs(h, W, y)
+    logp, ent, lse = grpo.lmhead_logprobs(h, W, y, chunk_rows=37888)
     rows = np.unique(np.concatenate([np.random.default_rng(0).integers(0, n, 40),
                                      [0, 127, 128, 37887, 37888, n - 1]]))
     rl, re, rs = LH.lmhead_forward(_bf16_np(h[rows]), _bf16_np(W), y[rows].cpu().numpy(),
