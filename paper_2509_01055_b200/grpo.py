@@ -172,6 +172,39 @@ class GRPOStep:
         per micro-batch with the step's global norm_groups / norm_tokens and
         accumulate_dweight=True after the first (outputs["dweight"] reused),
         then combine the reports with parallel.combine_reports."""
+        plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
+                             backward=backward, norm_groups=norm_groups, norm_tokens=norm_tokens,
+                             outputs=outputs, adv_cache=adv_cache,
+                             accumulate_dweight=accumulate_dweight)
+        self._launch(plan, stream)
+        return plan.result(sync_report)
+
+    def capture(self, packed: PackedBatch, group_off, rewards, hidden, weight, logp_old,
+                logp_ref=None, *, norm_groups: float | None = None,
+                norm_tokens: float | None = None, outputs=None) -> "CapturedStep":
+        """Record the whole device side of a step (advantages + fused LM-head
+        step + reductions) as one CUDA graph.  Every argument becomes a
+        static buffer: refill packed / hidden / logp / rewards tensors in place
+        (same shapes) and call replay().  rewards must be a device tensor."""
+        import torch
+
+        plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
+                             backward=True, norm_groups=norm_groups, norm_tokens=norm_tokens,
+                             outputs=outputs, adv_cache=None, accumulate_dweight=False)
+        if plan.rewards.data_ptr() != getattr(rewards, "data_ptr", lambda: -1)():
+            raise ValueError("capture() needs rewards as a float64 device tensor (static input)")
+        side = torch.cuda.Stream(device=hidden.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up (occupancy queries, lazy loads) off-capture
+            self._launch(plan, None)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self._launch(plan, None)
+        return CapturedStep(graph, plan)
+
+    def _prepare(self, packed, group_off, rewards, hidden, weight, logp_old, logp_ref, *,
+                 backward, norm_groups, norm_tokens, outputs, adv_cache, accumulate_dweight):
         import torch
 
         L = _lib.lib()
@@ -190,50 +223,100 @@ class GRPOStep:
         agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
         go = np.asarray(group_off, dtype=np.int32)
         n_groups = len(go) - 1
+        plan = _StepPlan()
+        plan.L = L
         if adv_cache is None:
-            adv64, adv32, traj_w, _tg, d_go = advantages(
-                rewards, go, std_floor=cfg.std_floor, agg=agg, norm_groups=norm_groups,
-                norm_tokens=norm_tokens if norm_tokens is not None else max(packed.n_act, 1),
-                act_off=packed.act_off, device=dev, stream=stream)
+            sizes = _group_sizes(go)
+            if np.any(sizes < 2):
+                from .errors import GroupTooSmall
+
+                g = int(np.argmax(sizes < 2))
+                raise GroupTooSmall(f"group {g}: need at least 2 rewards, got {int(sizes[g])}")
+            B = int(go[-1])
+            r = rewards if torch.is_tensor(rewards) else torch.from_numpy(
+                np.ascontiguousarray(np.asarray(rewards, dtype=np.float64)))
+            plan.rewards = r.to(device=dev, dtype=torch.float64)
+            plan.d_go = torch.from_numpy(go).to(dev)
+            plan.adv64 = torch.empty(B, dtype=torch.float64, device=dev)
+            plan.adv32 = torch.empty(B, dtype=torch.float32, device=dev)
+            plan.traj_w = torch.empty(B, dtype=torch.float32, device=dev)
+            plan.tgroup = torch.empty(B, dtype=torch.int32, device=dev)
+            nt = norm_tokens if norm_tokens is not None else max(packed.n_act, 1)
+            plan.adv_args = (plan.rewards.data_ptr(), plan.d_go.data_ptr(), n_groups, B,
+                             cfg.std_floor, _lib.ptr(packed.act_off), agg,
+                             float(norm_groups if norm_groups is not None else n_groups),
+                             float(nt), plan.adv64.data_ptr(), plan.adv32.data_ptr(),
+                             plan.traj_w.data_ptr(), plan.tgroup.data_ptr())
         else:
-            adv64, adv32, traj_w, d_go = adv_cache
+            plan.adv64, plan.adv32, plan.traj_w, plan.d_go = adv_cache
+            plan.adv_args = None
         T = packed.n_tokens
         out = outputs or {}
-        logp = out.get("logp")
-        if logp is None:
-            logp = torch.empty(max(T, 1), dtype=torch.float32, device=dev)
-        ent = out.get("entropy")
-        if ent is None:
-            ent = torch.empty(max(T, 1), dtype=torch.float32, device=dev)
-        dh = dw = None
-        if backward:
-            dh = out.get("dhidden")
-            if dh is None:
-                dh = torch.empty((T, self.H), dtype=torch.bfloat16, device=dev)
-            dw = out.get("dweight")
-            if dw is None:
-                dw = torch.empty((self.V, self.H), dtype=torch.float32, device=dev)
-        rep = out.get("report")
-        if rep is None:
-            rep = torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)
+
+        def buf(key, shape, dtype):
+            t = out.get(key)
+            return t if t is not None else torch.empty(shape, dtype=dtype, device=dev)
+
+        plan.T = T
+        plan.logp = buf("logp", max(T, 1), torch.float32)
+        plan.ent = buf("entropy", max(T, 1), torch.float32)
+        plan.dh = buf("dhidden", (T, self.H), torch.bfloat16) if backward else None
+        plan.dw = buf("dweight", (self.V, self.H), torch.float32) if backward else None
+        plan.rep = buf("report", _lib.TL_REPORT_LEN, torch.float64)
         chunk = self._chunk(packed.n_act, T, packed.n_traj, n_groups, dev)
         self.last_chunk = chunk
         ws_bytes = int(L.tl_lmhead_step_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
                                                         n_groups, self.mode))
-        ws = self._ws.get(ws_bytes, dev)
-        c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
-        _lib.check(L.tl_grpo_lmhead_step(
+        plan.ws = self._ws.get(ws_bytes, dev)
+        plan.cfg_c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
+        plan.keep = (packed, hidden, weight, logp_old, logp_ref)  # pointers stay valid
+        plan.step_args = (
             hidden.data_ptr(), weight.data_ptr(), packed.input_ids.data_ptr(),
             packed.loss_mask.data_ptr(), packed.act_idx.data_ptr(), packed.n_act,
-            packed.traj_of_token.data_ptr(), packed.cu_seqlens.data_ptr(), d_go.data_ptr(),
-            logp_old.data_ptr(), _lib.ptr(logp_ref), adv32.data_ptr(), traj_w.data_ptr(), T,
-            self.H, self.V, packed.n_traj, n_groups, c, logp.data_ptr(), ent.data_ptr(),
-            _lib.ptr(dh), _lib.ptr(dw), rep.data_ptr(), chunk,
-            self.mode | (_lib.LMHEAD_ACCUMULATE_DW if accumulate_dweight else 0), ws.data_ptr(),
-            ws_bytes,
-            _lib.stream_handle(stream)))
-        return StepResult(report=report_dict(rep.cpu()) if sync_report else {}, report_tensor=rep, logp=logp[:T], entropy=ent[:T],
-                          dhidden=dh, dweight=dw, adv=adv64)
+            packed.traj_of_token.data_ptr(), packed.cu_seqlens.data_ptr(), plan.d_go.data_ptr(),
+            logp_old.data_ptr(), _lib.ptr(logp_ref), plan.adv32.data_ptr(),
+            plan.traj_w.data_ptr(), T, self.H, self.V, packed.n_traj, n_groups, plan.cfg_c,
+            plan.logp.data_ptr(), plan.ent.data_ptr(), _lib.ptr(plan.dh), _lib.ptr(plan.dw),
+            plan.rep.data_ptr(), chunk,
+            self.mode | (_lib.LMHEAD_ACCUMULATE_DW if accumulate_dweight else 0),
+            plan.ws.data_ptr(), ws_bytes)
+        return plan
+
+    @staticmethod
+    def _launch(plan, stream):
+        """Device work only (stream-ordered launches, no host sync): K2 then
+        the fused LM-head step; capturable."""
+        L = plan.L
+        s = _lib.stream_handle(stream)
+        if plan.adv_args is not None:
+            _lib.check(L.tl_group_advantages(*plan.adv_args, s))
+        _lib.check(L.tl_grpo_lmhead_step(*plan.step_args, s))
+
+
+class _StepPlan:
+    """Buffers and C-call arguments of one GRPOStep call (see _prepare)."""
+
+    def result(self, sync_report: bool = True) -> StepResult:
+        T = self.T
+        return StepResult(report=report_dict(self.rep.cpu()) if sync_report else {},
+                          report_tensor=self.rep, logp=self.logp[:T], entropy=self.ent[:T],
+                          dhidden=self.dh, dweight=self.dw, adv=self.adv64)
+
+
+class CapturedStep:
+    """A GRPO step recorded as one CUDA graph (GRPOStep.capture): replay()
+    re-runs advantages + fused LM-head forward / surrogate / backward +
+    reductions on the current contents of the captured input buffers."""
+
+    def __init__(self, graph, plan):
+        self.graph = graph
+        self.plan = plan
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def result(self, sync_report: bool = True) -> StepResult:
+        return self.plan.result(sync_report)
 
 
 def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_ref=None,

@@ -89,3 +89,25 @@ def test_pack_deterministic_under_arrival_order():
     for k in ("input_ids", "loss_mask", "position_ids", "cu_seqlens", "act_idx"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
     assert np.array_equal(a.act_off.cpu().numpy(), b.act_off.cpu().numpy())
+
+
+def test_captured_step_replays_eager_bitwise():
+    """GRPOStep.capture records the device side of a step (K2 + fused LM-head
+    step + reductions) as one CUDA graph; replay() on the captured buffers
+    equals the eager step bitwise, also after the inputs are refilled in
+    place."""
+    wl, H, V, packed, h, W, lold, lref = _tiny_step_inputs()
+    cfg = LossConfig(kl_beta=0.04, entropy_coef=0.01)
+    rw = torch.from_numpy(wl.rewards).cuda()
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=256)
+    cap = step.capture(packed, wl.group_off, rw, h, W, lold, lref)
+    for refill in (False, True):
+        if refill:  # new behaviour-policy log-probs and rewards, same shapes
+            lold.add_(0.01)
+            rw.copy_(rw.flip(0))
+        cap.replay()
+        got = _outputs(cap.result())
+        ref = _outputs(grpo.GRPOStep(H, V, cfg, chunk_rows=256)(
+            packed, wl.group_off, rw, h, W, lold, lref))
+        for x, y in zip(got, ref):
+            assert torch.equal(x, y)
