@@ -103,3 +103,42 @@ def test_finalize_report_matches_allreduce():
     ref = O.loss_report(groups, 0.2, 0.1)
     assert abs(fin[0] - ref["objective"]) <= 1e-12
     assert abs(fin[3] - ref["kl"]) <= 1e-12
+
+
+def test_combine_reports_micro_batches():
+    """Micro-batches of whole groups: combining their reports (additive
+    partials, then ratios) gives the one-shot report, in host and in device
+    (bench.combine_reports_device) form."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    groups = _batch(5, n_groups=12)
+    parts = [_report_partials(groups[a:b]) for a, b in ((0, 4), (4, 5), (5, 12))]
+    for p in parts:  # the kernels also emit the ratios; combine must recompute them
+        p[0] = p[11] / max(p[4], 1)
+    ref = O.loss_report(groups, 0.2, 0.1)
+    for rep in (parallel.combine_reports(parts, 0),
+                bench.combine_reports_device([torch.tensor(p) for p in parts], 0).numpy()):
+        assert rep[2] == ref["masked_tokens"] and rep[4] == ref["groups"]
+        assert abs(rep[0] - ref["objective"]) <= 1e-12
+        assert abs(rep[1] - ref["clip_fraction"]) <= 1e-12
+        assert abs(rep[3] - ref["kl"]) <= 1e-12
+
+
+def test_micro_batches_cover_groups_in_order():
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2509_01055_b200.synthetic import CONFIGS, group_tokens
+
+    cfg = CONFIGS["c3"]
+    groups = np.arange(0, cfg.prompts, 3)
+    mbs = bench.micro_batches(cfg, groups, 2_000_000)
+    assert np.array_equal(np.concatenate(mbs), groups)
+    toks = [int(group_tokens(cfg, m).sum()) for m in mbs]
+    assert len(mbs) > 1 and all(t <= 2_000_000 or len(m) == 1 for t, m in zip(toks, mbs))
