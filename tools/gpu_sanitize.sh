@@ -1,5 +1,5 @@
 # compute-sanitizer over the GPU parity tests (memcheck on the fused step incl. tcgen05 GEMMs; racecheck/synccheck on shared-memory kernels)
-K1='test_pack or test_advantages or test_loss_fp32 or test_grpo_lmhead_step_vs_oracle or microbatch or dapo'
+K1='test_pack or test_advantages or test_loss_fp32 or test_grpo_lmhead_step_vs_oracle or microbatch or dapo or split_k or no_action'
 K2='test_pack or test_advantages or test_loss_fp32 or test_grpo_lmhead_step_vs_oracle'
 for tool in memcheck racecheck synccheck; do
   k="$K1"; [ $tool != memcheck ] && k="$K2"
