@@ -416,8 +416,12 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   strips = strips < 1 ? 1 : (strips > kMaxStripsFwd ? kMaxStripsFwd : strips);
   const int strip = (n_tiles + strips - 1) / strips;
   const int group_m = env_int("TL_FWD_GROUPM", num_sms() / kCG / 2);
+  // L2 priorities: the wave's h_c rows are re-read for every W tile of the
+  // strip (evict_last); a W tile is used by the strip's pairs within one
+  // lockstep window and not again this wave (evict_first): -4.9 % forward
+  // (tools/experiments/gpu_r51).
   GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, env_int("TL_FWD_POLA", 2),
-                           env_int("TL_FWD_POLB", 0));
+                           env_int("TL_FWD_POLB", 1));
   // per-strip lockstep: a strip's 37 pairs (sharing its W tiles) wait on each
   // other only, not on the other strip of the wave
   return with_sync(s, sync, 8 * s.k_blocks, 1, "FWD", 1);
@@ -677,7 +681,11 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
         return e;
       // N-complete raster (group_m = 1): all H tiles of an M tile run together
       // so each dS k-block is fetched from HBM once; dS streams (evict first).
-      const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG, 0, 0),
+      // dS streams (evict_first); W is re-read by every wave and the
+      // serpentine order starts each wave on what the last one read
+      // (evict_last): -1.1 % dH (gpu_r50)
+      const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG,
+                                                env_int("TL_DH_POLA", 1), env_int("TL_DH_POLB", 2)),
                                      b.sync + 2 * kSyncWaves, 64, 1, "DH");
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
@@ -686,7 +694,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     }
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
-    GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, 0, 0),
+    // dS streams (evict_first), h_c is re-read by every wave (evict_last): -2.8 % dW
+    GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, env_int("TL_DW_POLA", 1),
+                                        env_int("TL_DW_POLB", 2)),
                              b.sync + 3 * kSyncWaves, 64, 1, "DW");
     if (env_int("TL_DW_TAIL", 1)) {  // split-K tail for the partial last wave
       sh.tail_part = b.tail_part;
