@@ -38,4 +38,4 @@ def main(prefix: str):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r1e")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1f")
