@@ -1,0 +1,9 @@
+# dS pass row order (2 reps)
+b() { n=$1; shift
+  env "$@" timeout 900 python bench.py --config c2 --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_$n.log 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/bench_$n.log').read().strip().splitlines()[-1]); print('$n', round(d['ms_per_step'],1), round(d['value']), d['clocks']['sm_mhz'], {k: round(v,1) for k,v in d['kernel_ms_per_step'].items() if v > 100})" || tail -5 gpurun_out/bench_$n.log
+}
+for r in 1 2; do
+b base_$r
+b rev_$r TL_DS_REVERSE=1
+done
