@@ -604,6 +604,7 @@ struct EpiStoreBF16 {
     __nv_bfloat16_raw* out;
     long long ldo;          // elements
     const int32_t* row_map; // nullable: out row = row_map[row]
+    int out_policy;         // make_policy() kind of the output stores
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -614,6 +615,7 @@ struct EpiStoreBF16 {
     const bool row_ok = row < s.M;
     long long orow = row;
     if (row_ok && p.row_map) orow = p.row_map[row];
+    const uint64_t pol = make_policy(p.out_policy);
     tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
       if (!row_ok) return;
       const int cb = col0 + c;
@@ -626,7 +628,7 @@ struct EpiStoreBF16 {
           v.y = pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
           v.z = pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
           v.w = pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
-          *reinterpret_cast<uint4*>(dst + j) = v;
+          st_v4_hint(dst + j, v, pol);
         }
       } else {
 #pragma unroll
@@ -654,6 +656,7 @@ struct EpiStoreF32 {
     long long ldo;
     int accumulate;
     int load_add;
+    int out_policy;  // make_policy() kind of the accumulate reductions
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -665,7 +668,8 @@ struct EpiStoreF32 {
     float* dst = p.out + static_cast<long long>(row) * p.ldo + col;
     if (col + 4 <= s.N) {
       if (p.accumulate && !p.load_add) {
-        red_add_v4_f32(dst, v);
+        if (p.out_policy) red_add_v4_f32_hint(dst, v, make_policy(p.out_policy));
+        else red_add_v4_f32(dst, v);
         return;
       }
       if (p.accumulate) {

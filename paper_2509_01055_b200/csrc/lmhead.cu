@@ -496,7 +496,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
   if (c_fp32 && N >= 1024) {  // wide 256 x 512 pair tiles (as the dH / dW GEMMs)
     const GemmShape s = make_shape(M, N, K, kBNWide, 1, kGroupM, kCG);
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0, 0};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
@@ -506,7 +506,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   }
   const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   if (c_fp32) {
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0, 0};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32>(ma, mb, s, ep, st);
@@ -515,7 +515,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
     }
   }
   TL_REQUIRE(!accumulate, TL_ERR_UNSUPPORTED, "accumulate needs fp32 C");
-  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr};
+  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr, 0};
   switch (sel) {
     case 0: return launch_gemm<kCG, false, false, EpiStoreBF16>(ma, mb, s, ep, st);
     case 1: return launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st);
@@ -687,7 +687,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG,
                                                 env_int("TL_DH_POLA", 1), env_int("TL_DH_POLB", 2)),
                                      b.sync + 2 * kSyncWaves, 64, 1, "DH");
-      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
+      // dhidden rows are written once and not read again in the step
+      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci,
+                              env_int("TL_DH_OUT_POLICY", 0)};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
         return e;
@@ -702,7 +704,8 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       sh.tail_part = b.tail_part;
       sh.tail_ctr = b.tail_ctr;
     }
-    EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0)};
+    EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0),
+                           env_int("TL_DW_OUT_POLICY", 0)};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };
 
