@@ -404,12 +404,13 @@ struct StreamPair {
 // is 2 strips x (n_pairs / 2) M-tiles, so the wave's h_c rows (37 x 256 x H
 // bf16 = 67 MB at C2) stay in L2 (evict_last) across the strip while every
 // W tile is fetched once per wave and shared by the n_pairs / 2 pairs of its
-// strip, kept close by the wave lockstep: sync steps of eight tiles, window
+// strip, kept close by the wave lockstep: sync steps of four tiles, window
 // 1 (a producer may not start step s before every CTA of its strip group has
-// issued step s-1).  Measured at C2 (tools/experiments/gpu_r17, r25, r30-r32):
-// one-tile window 2 -> 1 cut the forward's DRAM reads 33 -> 14 GB per chunk
-// (before serpentine K); per-strip instead of whole-wave groups -0.5 %;
-// 1 -> 2 -> 4 -> 8-tile steps -0.5 / -0.4 / -0.2 % (fewer waits).
+// issued step s-1).  Measured at C2 (tools/experiments/gpu_r17, r25, r30-r32,
+// r57): one-tile window 2 -> 1 cut the forward's DRAM reads 33 -> 14 GB per
+// chunk (before serpentine K); per-strip instead of whole-wave groups -0.5 %;
+// 1 -> 2 -> 4-tile steps -0.5 / -0.4 %; with W tiles evict_first the
+// forward depends on the lockstep more (none: +10.6 %) and 4 beats 8 by 0.3 %.
 GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int n_tiles = (V + kBN - 1) / kBN;
   int strips = env_int("TL_FWD_STRIPS", kStripsFwd);
@@ -424,7 +425,7 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
                            env_int("TL_FWD_POLB", 1));
   // per-strip lockstep: a strip's 37 pairs (sharing its W tiles) wait on each
   // other only, not on the other strip of the wave
-  return with_sync(s, sync, 8 * s.k_blocks, 1, "FWD", 1);
+  return with_sync(s, sync, 4 * s.k_blocks, 1, "FWD", 1);
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
