@@ -105,119 +105,89 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- CPU baseline --
-def cpu_baseline(cfg, wl, target_s: float = 12.0, threads: int | None = None):
-    """The reference's CPU path on a bounded sample of the same workload:
-    the oracle port of token_records -> group_advantages ->
-    grpo_multi_turn_loss (pure Python, as toolloop runs it) on one whole group,
-    plus the fp32 numpy LM-head restatement (fwd + bwd, multithreaded BLAS) on
-    a sample of action tokens; tokens/s extrapolated per token."""
-    from oracle import grpo_oracle as O
-    from oracle import lmhead_oracle as LH
+def workload_config(cfg, world: int, scaling: str) -> dict:
+    """The `config` object of both arms' JSON lines (workload only; the GPU
+    arm's implementation choices go to `impl_config`)."""
+    from paper_2509_01055_b200.synthetic import group_act_tokens, group_tokens
 
-    tab = wl.table
-    # --- loss path on group 0
-    b0, b1 = int(wl.group_off[0]), int(wl.group_off[1])
-    segs_all = []
-    pos_pool = tab.token_pool
-    cu = 0
-    starts = []
-    for b in range(b0, b1):
-        segs = []
-        for s in range(tab.traj_seg_off[b], tab.traj_seg_off[b + 1]):
-            o = int(tab.seg_src_off[s])
-            n = int(tab.seg_len[s])
-            segs.append(("action" if tab.seg_is_action[s] else "observation", pos_pool[o:o + n].tolist()))
-        segs_all.append(segs)
-    lens = [sum(len(t) for _, t in s) for s in segs_all]
-    tg = sum(lens)
-    new = (wl.logp_old[:tg] + 0.05).astype(np.float64)  # logp_new stand-in (LM head timed separately)
-    old = wl.logp_old[:tg].astype(np.float64)
-    ref = wl.logp_ref[:tg].astype(np.float64)
-    t0 = time.perf_counter()
-    recs, pos = [], 0
-    for s, n in zip(segs_all, lens):
-        recs.append(O.token_records(s, new[pos:pos + n].tolist(), old[pos:pos + n].tolist(),
-                                    ref[pos:pos + n].tolist()))
-        pos += n
-    adv = O.group_advantages(wl.rewards[b0:b1].tolist())
-    O.multi_turn(recs, adv, 0.2, 0.0)
-    t_loss = time.perf_counter() - t0
-    # --- LM head on a sample of action tokens
-    H, V = cfg.hidden, cfg.vocab
-    rng = np.random.default_rng(7)
-    W = LH.to_bf16_f32((rng.standard_normal((V, H), dtype=np.float32) * 0.02))
-    y = rng.integers(0, V, 4096)
+    n_groups = cfg.prompts * (world if scaling == "weak" else 1)
+    gids = np.arange(n_groups)
+    return {"workload": cfg.desc, "name": cfg.name, "global_batch": n_groups * cfg.n,
+            "seq_len": cfg.seq, "hidden": cfg.hidden, "vocab": cfg.vocab,
+            "tokens_per_step": int(group_tokens(cfg, gids).sum()),
+            "action_tokens_per_step": int(group_act_tokens(cfg, gids).sum()),
+            "loss_agg": cfg.loss_agg, "parallelism": f"dp{world} (groups, LPT)",
+            "l2": "inputs >> L2 (hidden is GBs)"}
 
-    def run(n):
-        h = LH.to_bf16_f32(rng.standard_normal((n, H), dtype=np.float32))
-        t = time.perf_counter()
-        LH.lmhead_forward(h, W, y[:n], chunk=128)
-        LH.lmhead_backward(h, W, y[:n], np.full(n, -1e-3), None, chunk=128)
-        return time.perf_counter() - t
 
-    # time(n) = fixed (dW alloc/accumulate over V x H) + n * per_token: take the
-    # slope between two sample sizes so the per-step fixed cost (amortised over
-    # a whole batch in a real step) does not inflate the per-token figure.
-    n1 = 64
-    run(n1)  # warm BLAS / page in W
-    t1 = run(n1)
-    n = int(min(4096, max(4 * n1, n1 * target_s / max(t1, 1e-3))))
-    dt = run(n)
-    per_act = max((dt - t1) / (n - n1), dt / n * 0.5)
-    f_act = wl.n_act / max(wl.n_tokens, 1)
-    per_tok = t_loss / tg + f_act * per_act
+def _calibrated_sampler(cfg, target_s: float):
+    """ReferenceSampler whose LM-head block takes ~target_s per sample."""
+    import bench_reference as R
+
+    smp = R.ReferenceSampler(cfg, lm_rows=64)
+    rate = 64 / smp.lm.run(64)
+    smp.lm_rows = int(min(4096, max(64, round(rate * target_s / 64) * 64)))
+    return smp
+
+
+def cpu_baseline(cfg, target_s: float = 8.0) -> dict:
+    """The reference's CPU path timed on a bounded sample (bench_reference):
+    rank 0, N = 1, one ~10-30 s sample."""
+    import bench_reference as R
+
+    smp = _calibrated_sampler(cfg, target_s)
     try:
-        from threadpoolctl import threadpool_info
-
-        blas_threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        blas_threads = os.cpu_count() or 1
-    return {
-        "value": 1.0 / per_tok,
-        "unit": UNIT,
-        "cores": int(blas_threads),
-        "kind": "port",
-        "sample": (f"oracle/ port: pure-Python token_records+group_advantages+multi_turn on group 0 "
-                   f"({tg} tokens, {t_loss:.3f}s, 1 core) + numpy fp32 LM-head fwd+bwd on {n} action "
-                   f"tokens at H={H} V={V} ({dt:.2f}s, {blas_threads} BLAS threads); "
-                   f"per-token cost extrapolated with f_act={f_act:.3f}"),
-        "host_cpu": _cpu_model(),
-    }
-
-
-def _cpu_model() -> str:
-    try:
-        for line in Path("/proc/cpuinfo").read_text().splitlines():
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
-    except Exception:
-        pass
-    return f"{os.cpu_count()} cpus"
+        st = smp.step()
+    finally:
+        smp.close()
+    return {"value": st["value"], "unit": UNIT, "cores": R.n_cores(), "kind": smp.kind,
+            "sample": smp.describe(st), "extrapolated_step_ms": st["extrapolated_step_ms"],
+            "host_cpu": R.cpu_model()}
 
 
 def run_reference(args, cfg):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from paper_2509_01055_b200.synthetic import make_workload
+    """--impl reference: the reference's own CPU implementation of the path
+    (bench_reference.py) on the host cores, rank 0 only (other ranks exit
+    0).  A step = one bounded sample of the workload (loss path on whole
+    groups, single-process and fanned out over every core; the LM head on a
+    block of action rows sized to ~--ref-seconds); `value` = the workload's
+    tokens/s extrapolated from the sample's per-token costs (median over
+    steps), `ms_per_step` = the measured wall time of one sample, and
+    `extrapolated_step_ms` = the whole configured step at that rate."""
+    import bench_reference as R
 
-    wl = make_workload(cfg, group_ids=np.arange(min(cfg.prompts, 2)))
-    for _ in range(args.warmup):
-        cpu_baseline(cfg, wl, target_s=3.0)
-    vals, last = [], None
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        last = cpu_baseline(cfg, wl, target_s=args.ref_seconds)
-        vals.append(last["value"])
-    wall = time.perf_counter() - t0
-    v = float(np.median(vals))
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    smp = _calibrated_sampler(cfg, args.ref_seconds)
+    try:
+        for _ in range(args.warmup):
+            smp.step()
+        res = []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res.append(smp.step())
+        wall = time.perf_counter() - t0
+        # the LM-head restatement on a 4096-row block once, for its GFLOP/s
+        t_lm = smp.lm.run(4096)
+    finally:
+        smp.close()
+    v = float(np.median([r["value"] for r in res]))
+    last = res[-1]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (loss path) / f32 (LM head)",
-        "data": "synthetic", "config": {"workload": cfg.desc, "name": cfg.name},
-        "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+        "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64 (reference loss path) / f32 (LM head restatement)", "data": "synthetic",
+        "config": workload_config(cfg, world, args.scaling),
+        "extrapolated_step_ms": float(np.median([r["extrapolated_step_ms"] for r in res])),
+        "ms_per_step_note": "wall time of one bounded sample; extrapolated_step_ms = the whole "
+                            "configured step at the sampled per-token rates",
+        "lm_head_4096_rows": {"s": t_lm, "gflops": 6.0 * 4096 * cfg.hidden * cfg.vocab / t_lm / 1e9,
+                              "threads": R.n_cores()},
+        "cpu_baseline": {"kind": smp.kind, "cores": R.n_cores(), "sample": smp.describe(last),
+                         "value": v, "unit": UNIT, "host_cpu": R.cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -261,6 +231,25 @@ def combine_reports_device(reps, agg: int):
     return tot
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _relaunch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-exec this command as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -268,6 +257,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank owns a full config-sized batch (global batch = N x config); "
+                         "strong: the config's batch is split across the N ranks")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -279,6 +271,12 @@ def main():
                     help="LM-head backward schedule (TL_LMHEAD_* in include/toolloop_b200.h); "
                          "store is fastest on a power-capped B200 (DESIGN.md §3)")
     args = ap.parse_args()
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     from paper_2509_01055_b200.synthetic import CONFIGS
 
@@ -294,7 +292,6 @@ def main():
     from paper_2509_01055_b200.rl.loss import AGG_TOKEN_MEAN, LossConfig
     from paper_2509_01055_b200.synthetic import group_act_tokens, make_workload
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # TL_BENCH_ONE_DEVICE=1 + TL_BENCH_BACKEND=gloo: every rank on cuda:0 over
@@ -304,15 +301,24 @@ def main():
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         backend = os.environ.get("TL_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init lines (nranks, NVLS / channels) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
+            # the step's own collectives (N1 report, N2 dW) go through the
+            # library's NCCL communicator at the C ABI (tl_nccl_*)
+            comm = parallel.NcclComm.from_process_group()
         else:
             dist.init_process_group(backend)
 
-    # global batch = world x config (weak scaling); whole groups per rank by LPT
-    n_groups_global = cfg.prompts * world
+    # global batch: world x config (weak) or the config split across ranks
+    # (strong); whole groups per rank by LPT
+    n_groups_global = cfg.prompts * (world if args.scaling == "weak" else 1)
     work = group_act_tokens(cfg, np.arange(n_groups_global))
     shards = parallel.shard_groups(work, world)
     agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
@@ -378,7 +384,10 @@ def main():
                        sync_report=False, accumulate_dweight=i > 0)
             reps.append(res.report_tensor)
         rep = reps[0] if len(reps) == 1 else combine_reports_device(reps, agg)
-        if world > 1:
+        if comm is not None:     # N1 + N2 at the C ABI (NCCL), stream-ordered
+            comm.allreduce_report(rep, agg)
+            comm.allreduce_grad(dweight)
+        elif world > 1:          # gloo process group (ranks sharing one GPU)
             parallel.allreduce_report(rep, agg)
             parallel.allreduce_grad(dweight)
         return rep
@@ -463,6 +472,8 @@ def main():
                          "hidden states / LM-head weight device-resident (model tensors)"}
 
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -497,18 +508,20 @@ def main():
             "step_frac": (flops_alg / (peak_s * 1e12)) / (ms / 1e3),
             "peak_kind": f"{peak_kind} bf16 sustained",
         }
+    wcfg = workload_config(cfg, world, args.scaling)
+    assert wcfg["tokens_per_step"] == int(T_all) and wcfg["action_tokens_per_step"] == int(A_all)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg.desc, "name": cfg.name, "global_batch": cfg.prompts * cfg.n * world,
-                   "seq_len": cfg.seq, "hidden": H, "vocab": V,
-                   "tokens_per_step": int(T_all), "action_tokens_per_step": int(A_all),
-                   "action_tokens_per_s": A_all / (ms / 1e3),
-                   "parallelism": f"dp{world} (groups, LPT)", "l2": "inputs >> L2 (hidden is GBs)",
-                   "chunk_rows": step.last_chunk, "loss_agg": cfg.loss_agg,
-                   "micro_batches": len(mbs),
-                   "lmhead_mode": args.mode},
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": wcfg,
+        "impl_config": {"action_tokens_per_s": A_all / (ms / 1e3),
+                        "collectives": ("NCCL at the C ABI (tl_allreduce_report, tl_allreduce_f32)"
+                                        if comm is not None else
+                                        ("torch.distributed " + dist.get_backend()) if world > 1
+                                        else "none"),
+                        "chunk_rows": step.last_chunk, "micro_batches": len(mbs),
+                        "lmhead_mode": args.mode},
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -517,8 +530,10 @@ def main():
         "report": {k: rep[k] for k in ("objective", "clip_fraction", "masked_tokens", "kl")},
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, wl)
+        line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

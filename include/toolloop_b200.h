@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TL_ABI_VERSION 1
+#define TL_ABI_VERSION 2  /* 2: tl_loss_config.entropy_norm, NCCL collectives */
 
 typedef void* tl_stream_t; /* cudaStream_t */
 
@@ -40,7 +40,8 @@ typedef enum tl_status {
   TL_ERR_CUDA = 4,
   TL_ERR_UNSUPPORTED = 5,
   TL_ERR_WORKSPACE = 6,
-  TL_ERR_EPISODE_LOG = 7      /* errors.EpisodeLogError (errors.py:44), "path:line: ..." */
+  TL_ERR_EPISODE_LOG = 7,     /* errors.EpisodeLogError (errors.py:44), "path:line: ..." */
+  TL_ERR_COMM = 8             /* NCCL unavailable or a collective failed           */
 } tl_status;
 
 const char* tl_last_error(void);
@@ -149,6 +150,11 @@ typedef struct tl_loss_config {
   int32_t has_ref;     /* logp_ref present                              */
   int32_t objective;   /* 0 clipped (A11/A13), 1 unclipped (A14)        */
   int32_t agg;         /* 0 seq-mean-token-mean (reference), 1 token-mean */
+  double entropy_norm; /* LM-head step: the entropy bonus is entropy_coef *
+                          sum(entropy) / entropy_norm, i.e. the mean over the
+                          step's GLOBAL action tokens when the step is split
+                          into micro-batches or data-parallel shards
+                          (<= 0: this call's action tokens)              */
 } tl_loss_config;
 
 /* Per-group result row of the fp64 parity path (TL_GROUP_OUT_LEN doubles):
@@ -227,6 +233,9 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
  * (micro-batches of one optimizer step; pass the step's global norm_groups /
  * norm_tokens to tl_group_advantages so every micro-batch scales alike). */
 #define TL_LMHEAD_ACCUMULATE_DW 0x100
+/* Debug flag OR-ed into `mode`: run the dW GEMM's partial last wave unsplit
+ * (no split-K tail); results agree to fp32 summation order (tests). */
+#define TL_LMHEAD_NO_SPLIT_TAIL 0x200
 /* Workspace for tl_grpo_lmhead_step in `mode` (PIPELINED holds two chunks). */
 size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
                                       int64_t n_tokens, int32_t n_traj, int32_t n_groups,
@@ -299,6 +308,38 @@ int tl_tokenize_segments(const tl_tokenizer* tok, const uint8_t* text, const int
  * total bytes; copied into out only if they fit in cap (out NULL: size only). */
 int tl_tokenizer_decode(const tl_tokenizer* tok, const int32_t* ids, int64_t n, uint8_t* out,
                         int64_t cap, int64_t* len);
+
+/* ------------------------------------------------------------------------
+ * N1 / N2 — data-parallel collectives (NCCL, stream-ordered).
+ * Replaces the serial per-group loop + aggregation of cli.loss
+ * (cli.py:317-344; groups are independent): each rank runs the
+ * step on its own whole groups with the global normalisers, then
+ *   N1  tl_allreduce_report: the TL_REPORT_LEN report summed over ranks
+ *       (additive partials) and its ratio fields recomputed, in place;
+ *   N2  tl_allreduce_f32 (dW, in place) or tl_reduce_scatter_f32 (dW row
+ *       shard [V / nranks, H] when W is partitioned).
+ * `comm` is an ncclComm_t (void*): create one with tl_nccl_unique_id on one
+ * rank, broadcast the id, tl_nccl_comm_init on every rank (current device),
+ * or pass a communicator the caller already owns.  NCCL is loaded at run
+ * time (libnccl.so.2); without it these return TL_ERR_COMM and
+ * tl_nccl_available() is 0.
+ * ---------------------------------------------------------------------- */
+#define TL_NCCL_UNIQUE_ID_BYTES 128
+int tl_nccl_available(void);
+int tl_nccl_version(void);
+int tl_nccl_unique_id(uint8_t* id_out /* TL_NCCL_UNIQUE_ID_BYTES */);
+int tl_nccl_comm_init(void** comm_out, const uint8_t* id, int32_t nranks, int32_t rank);
+int tl_nccl_comm_destroy(void* comm);
+int tl_nccl_comm_size(void* comm, int32_t* nranks);
+/* sum of n doubles over ranks, in place (SURVEY §8(b) tl_allreduce_scalars) */
+int tl_allreduce_scalars(void* comm, double* x, int32_t n, tl_stream_t stream);
+/* N1: report[TL_REPORT_LEN] of each rank -> the global report (agg as tl_loss_config.agg) */
+int tl_allreduce_report(void* comm, double* report, int32_t agg, tl_stream_t stream);
+/* N2: dW all-reduce (in place) / reduce-scatter (rank r receives elements
+ * [r * shard_n, (r + 1) * shard_n) of the sum; buf holds nranks * shard_n) */
+int tl_allreduce_f32(void* comm, float* buf, int64_t n, tl_stream_t stream);
+int tl_reduce_scatter_f32(void* comm, const float* buf, float* shard, int64_t shard_n,
+                          tl_stream_t stream);
 
 /* Plain tcgen05 GEMM (building block, exported for tests):
  * C[M,N] (+)= A[M,K] * B[N,K]^T with A given K-major ([M,K], lda) or MN-major

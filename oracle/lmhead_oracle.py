@@ -64,6 +64,51 @@ def lmhead_forward(h: np.ndarray, W: np.ndarray, y: np.ndarray, chunk: int = 512
     return logp, ent, lse
 
 
+def lmhead_fwd_bwd_f64(h, W, y, g_fn, c, chunk: int = 4096):
+    """The same equations in torch float64 on whatever device h / W live on
+    (large-shape checker for the GPU tests: C2 / C5 vocab at tens of
+    thousands of rows is hours in numpy).  h [T, H], W [V, H] bf16 tensors,
+    y [T] int.  The upstream gradients may depend on the forward: g_fn(logp)
+    -> g [T] (float64 tensor), c scalar or [T] tensor = dLoss/dent.  Returns
+    (logp, ent, lse, dH, dW) in float64; dS is kept in float64 (no rounding),
+    so dH / dW are the exact-arithmetic gradients of the bf16 inputs."""
+    import torch
+
+    T = h.shape[0]
+    dev = h.device
+    W64 = W.to(torch.float64)
+    y = y.to(device=dev, dtype=torch.long)
+    logp = torch.empty(T, dtype=torch.float64, device=dev)
+    ent = torch.empty_like(logp)
+    lse = torch.empty_like(logp)
+    ez = torch.empty_like(logp)
+    for s in range(0, T, chunk):
+        e = min(T, s + chunk)
+        z = h[s:e].to(torch.float64) @ W64.T
+        l = torch.logsumexp(z, dim=1)
+        p = torch.exp(z - l[:, None])
+        lse[s:e] = l
+        logp[s:e] = z.gather(1, y[s:e, None])[:, 0] - l
+        ez[s:e] = (p * z).sum(1)
+        ent[s:e] = l - ez[s:e]
+        del z, p
+    g = g_fn(logp).to(device=dev, dtype=torch.float64)
+    c = torch.as_tensor(c, dtype=torch.float64, device=dev).expand(T)
+    dH = torch.empty((T, W.shape[1]), dtype=torch.float64, device=dev)
+    dW = torch.zeros_like(W64)
+    for s in range(0, T, chunk):
+        e = min(T, s + chunk)
+        hs = h[s:e].to(torch.float64)
+        z = hs @ W64.T
+        p = torch.exp(z - lse[s:e, None])
+        dz = -g[s:e, None] * p - c[s:e, None] * p * (z - ez[s:e, None])
+        dz[torch.arange(e - s, device=dev), y[s:e]] += g[s:e]
+        dH[s:e] = dz @ W64
+        dW += dz.T @ hs
+        del z, p, dz
+    return logp, ent, lse, dH, dW
+
+
 def lmhead_backward(h, W, y, g, c=None, chunk: int = 512):
     """Returns dH [T, H] fp32 and dW [V, H] fp32 for per-token upstream grads
     g = dLoss/dlogp and c = dLoss/dent (None -> 0)."""

@@ -41,8 +41,8 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = BUILD / (src.stem + ".o")
+def _compile(src: Path, verbose: bool, build_dir: Path = BUILD, extra=()) -> Path:
+    obj = build_dir / (src.stem + ".o")
     deps = [src] + _headers()
     if not _stale(obj, deps):
         return obj
@@ -50,33 +50,39 @@ def _compile(src: Path, verbose: bool) -> Path:
         cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall",
                f"-I{ROOT / 'include'}", "-c", str(src), "-o", str(obj)]
     else:
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")
-    (BUILD / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+    (build_dir / (src.stem + ".ptxas.txt")).write_text(res.stderr)
     if verbose:
         print(f"[build] {src.name}", file=sys.stderr)
     return obj
 
 
-def build(force: bool = False, verbose: bool = True) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = True, variant: str | None = None,
+          extra_flags=()) -> Path:
+    """Build the library.  variant="name" + extra_flags: an A/B build of the
+    same sources into _objs/<name>/libtoolloop_b200.so (selected at run time
+    with TOOLLOOP_B200_LIB=<path>); the product library is untouched."""
+    build_dir = BUILD / variant if variant else BUILD
+    lib = build_dir / LIB.name if variant else LIB
+    build_dir.mkdir(parents=True, exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
     if force:
-        for o in BUILD.glob("*.o"):
+        for o in build_dir.glob("*.o"):
             o.unlink()
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
-               "-lpthread"]
+        objs = list(ex.map(lambda s: _compile(s, verbose, build_dir, tuple(extra_flags)), srcs))
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
+               "-lpthread", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")
         if verbose:
-            print(f"[build] linked {LIB.name}", file=sys.stderr)
-    return LIB
+            print(f"[build] linked {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":

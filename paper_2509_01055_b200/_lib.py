@@ -8,13 +8,18 @@ ExtensionMissing — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import ExtensionMissing, GroupTooSmall, MaskMismatch, ToolloopError
 
 LIB_PATH = Path(__file__).resolve().parent / "libtoolloop_b200.so"
+# A/B builds of the same library (tools/*_ab.py) are selected by path
+if os.environ.get("TOOLLOOP_B200_LIB"):
+    LIB_PATH = Path(os.environ["TOOLLOOP_B200_LIB"])
 
+TL_ABI_VERSION = 2  # include/toolloop_b200.h
 TL_OK = 0
 TL_ERR_INVALID_ARG = 1
 TL_ERR_MASK_MISMATCH = 2
@@ -23,6 +28,8 @@ TL_ERR_CUDA = 4
 TL_ERR_UNSUPPORTED = 5
 TL_ERR_WORKSPACE = 6
 TL_ERR_EPISODE_LOG = 7
+TL_ERR_COMM = 8
+TL_NCCL_UNIQUE_ID_BYTES = 128
 TL_GROUP_OUT_LEN = 8
 TL_REPORT_LEN = 12
 
@@ -40,6 +47,9 @@ EXPORTS = [
     "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
     "tl_tokenizer_create", "tl_tokenizer_free", "tl_tokenizer_vocab_size",
     "tl_tokenize_segments", "tl_tokenizer_decode",
+    "tl_nccl_available", "tl_nccl_version", "tl_nccl_unique_id", "tl_nccl_comm_init",
+    "tl_nccl_comm_destroy", "tl_nccl_comm_size", "tl_allreduce_scalars", "tl_allreduce_report",
+    "tl_allreduce_f32", "tl_reduce_scatter_f32",
 ]
 
 
@@ -47,7 +57,7 @@ class LossConfigC(C.Structure):
     _fields_ = [
         ("eps_low", C.c_double), ("eps_high", C.c_double), ("kl_beta", C.c_double),
         ("entropy_coef", C.c_double), ("use_mask", C.c_int32), ("has_ref", C.c_int32),
-        ("objective", C.c_int32), ("agg", C.c_int32),
+        ("objective", C.c_int32), ("agg", C.c_int32), ("entropy_norm", C.c_double),
     ]
 
 
@@ -104,6 +114,16 @@ _SIGS = {
     "tl_tokenizer_vocab_size": (_I32, [_P]),
     "tl_tokenize_segments": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P, _I32]),
     "tl_tokenizer_decode": (C.c_int, [_P, _P, _I64, _P, _I64, C.POINTER(_I64)]),
+    "tl_nccl_available": (C.c_int, []),
+    "tl_nccl_version": (C.c_int, []),
+    "tl_nccl_unique_id": (C.c_int, [_P]),
+    "tl_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), _P, _I32, _I32]),
+    "tl_nccl_comm_destroy": (C.c_int, [_P]),
+    "tl_nccl_comm_size": (C.c_int, [_P, C.POINTER(_I32)]),
+    "tl_allreduce_scalars": (C.c_int, [_P, _P, _I32, _P]),
+    "tl_allreduce_report": (C.c_int, [_P, _P, _I32, _P]),
+    "tl_allreduce_f32": (C.c_int, [_P, _P, _I64, _P]),
+    "tl_reduce_scatter_f32": (C.c_int, [_P, _P, _P, _I64, _P]),
 }
 
 _lock = threading.Lock()
@@ -124,6 +144,10 @@ def load(require_device: bool = True) -> C.CDLL:
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            if lib.tl_abi_version() != TL_ABI_VERSION:
+                raise ExtensionMissing(
+                    f"{LIB_PATH} has ABI {lib.tl_abi_version()}, this package needs "
+                    f"{TL_ABI_VERSION}: rebuild it (__graft_entry__.build())")
             _lib = lib
     if require_device:
         import torch
@@ -175,6 +199,7 @@ LMHEAD_STORE_LOGITS = 0
 LMHEAD_RECOMPUTE = 1
 LMHEAD_STORE_LOGITS_PIPELINED = 2
 LMHEAD_ACCUMULATE_DW = 0x100
+LMHEAD_NO_SPLIT_TAIL = 0x200
 
 
 def profile_enable(on: bool = True) -> None:

@@ -106,6 +106,11 @@ struct GemmShape {
   // the previous tile (of this CTA and, in lockstep, of its whole wave) read
   // last — still in L2 when the operand is too large to stay resident.  Only
   // the producer's block order changes (fixed per tile: deterministic).
+  // serpentine == 2: parity of the global N tile instead (strip shapes: a
+  // CTA still alternates along its strip), so an output element's K order —
+  // and its fp32 bits — do not depend on which M tile / wave / chunk its row
+  // landed in (the LM-head forward: per-row outputs invariant under
+  // chunking and data-parallel sharding).
   int serpentine;
   // Split-K tail (strip == 1 shapes, epilogues with Epi::kSplitTail; set by
   // the launcher once it knows the number of co-resident pairs): the units of
@@ -353,7 +358,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // sub-MMA j covers tile columns [j*kUmmaN, (j+1)*kUmmaN); this CTA
           // stages rows rank*kBRows.. of each (the pair MMA splits B in half)
           const int n0 = (uc.n_begin + t) * BN + static_cast<int>(rank) * Smem::kBRows;
-          const bool rev = shape.serpentine && ((wave + t) & 1);
+          const bool rev = shape.serpentine == 2 ? ((uc.n_begin + t) & 1)
+                                                 : (shape.serpentine && ((wave + t) & 1));
           for (int kb = 0; kb < nkb; ++kb) {
             if (ctr && do_wait && in_step == 0 && sstep >= shape.sync_window) {
               // The lockstep only shapes L2 reuse, never correctness: a wait that
@@ -604,7 +610,6 @@ struct EpiStoreBF16 {
     __nv_bfloat16_raw* out;
     long long ldo;          // elements
     const int32_t* row_map; // nullable: out row = row_map[row]
-    int out_policy;         // make_policy() kind of the output stores
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -615,7 +620,6 @@ struct EpiStoreBF16 {
     const bool row_ok = row < s.M;
     long long orow = row;
     if (row_ok && p.row_map) orow = p.row_map[row];
-    const uint64_t pol = make_policy(p.out_policy);
     tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
       if (!row_ok) return;
       const int cb = col0 + c;
@@ -628,7 +632,7 @@ struct EpiStoreBF16 {
           v.y = pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
           v.z = pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
           v.w = pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
-          st_v4_hint(dst + j, v, pol);
+          *reinterpret_cast<uint4*>(dst + j) = v;
         }
       } else {
 #pragma unroll
@@ -644,19 +648,17 @@ struct EpiStoreBF16 {
 };
 
 // fp32 store or accumulate (out += acc), used for dW across token chunks.
-// Accumulation is a fire-and-forget vector reduction at L2 (red.add.v4.f32)
-// unless `load_add` is set (load + add + store): the dW tile is BN = 512 wide
-// and single-buffered in TMEM, so an epilogue waiting on 512 loads per row
-// would stall the next tile's MMAs.  Each element has one writer per launch,
-// so both forms give the same bits.
+// Accumulation is a fire-and-forget vector reduction at L2 (red.add.v4.f32):
+// the dW tile is BN = 512 wide and single-buffered in TMEM, so an epilogue
+// waiting on 512 loads per row (load + add + store) would stall the next
+// tile's MMAs (dW -7 % per chunk).  Each element has one writer per launch,
+// so the result is deterministic.
 struct EpiStoreF32 {
   static constexpr bool kSplitTail = true;
   struct Params {
     float* out;
     long long ldo;
     int accumulate;
-    int load_add;
-    int out_policy;  // make_policy() kind of the accumulate reductions
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -667,19 +669,10 @@ struct EpiStoreF32 {
     if (row >= s.M) return;
     float* dst = p.out + static_cast<long long>(row) * p.ldo + col;
     if (col + 4 <= s.N) {
-      if (p.accumulate && !p.load_add) {
-        if (p.out_policy) red_add_v4_f32_hint(dst, v, make_policy(p.out_policy));
-        else red_add_v4_f32(dst, v);
-        return;
-      }
-      if (p.accumulate) {
-        const float4 o = *reinterpret_cast<const float4*>(dst);
-        v.x += o.x;
-        v.y += o.y;
-        v.z += o.z;
-        v.w += o.w;
-      }
-      *reinterpret_cast<float4*>(dst) = v;
+      if (p.accumulate)
+        red_add_v4_f32(dst, v);
+      else
+        *reinterpret_cast<float4*>(dst) = v;
     } else {
       const float e[4] = {v.x, v.y, v.z, v.w};
       for (int j = 0; j < 4; ++j)

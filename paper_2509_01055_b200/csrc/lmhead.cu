@@ -13,8 +13,10 @@
 //               (lse, logp = z_y - lse, entropy) and runs the GRPO surrogate
 //               (grpo_token.cuh) on logp_new in the same epilogue: per-token
 //               term / k3 / flags and dLoss/dlogp, dLoss/dent.  In store mode
-//               the epilogue also writes the chunk's logits as fp16.
-//   dsoftmax    (store mode) fp16 z -> bf16 dS in place, HBM-bound
+//               the epilogue also writes the chunk's logits as fp16
+//               u = (z - m) log2e <= 0 with an int16 offset m per 32 columns
+//               (lmhead_epilogue.cuh).
+//   dsoftmax    (store mode) fp16 u -> bf16 dS in place, HBM-bound
 //   recompute   (recompute mode) same GEMM, epilogue writes dS (bf16, [C, V])
 //               dS = g (onehot(y) - p) - c p (z - E_p z),  p = e^(z - lse)
 //   dH GEMM     dhidden[act_idx] = dS W          (A K-major, B = W MN-major)
@@ -28,7 +30,6 @@
 #include <cuda_fp16.h>
 
 #include <mutex>
-#include <string>
 
 #include "gemm_sm100.cuh"
 #include "grpo_token.cuh"
@@ -49,7 +50,6 @@ constexpr int kBNWide = 512;
 constexpr int kStages = TL_STAGES256;  // ring depth of the 256-wide tiles (32 KB stages;
                                        // 7 = 224 KB, -0.2 % vs 6 at C2, gpu_r48)
 constexpr int kStripsFwd = 6;  // even: a wave covers 2 strips of one M group
-constexpr int kMaxStripsFwd = 16;  // partials capacity (TL_FWD_STRIPS profiling override)
 constexpr int kGroupM = 16;
 
 // ------------------------------------------------------------------ TMA maps --
@@ -114,6 +114,7 @@ unsigned long long* h_stats_base = nullptr;  // [PROF categories][160 CTAs][8]
 
 // split-K tail slice buffer: tile halves of 128 rows x 512 fp32 columns
 constexpr int kTailSlots = 160;
+constexpr int kMaxDevices = 64;
 
 template <int CG, bool A_MN, bool B_MN, class Epi, int BN = kBN>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
@@ -135,17 +136,28 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   lc.numAttrs = 1;
   // Persistent grid: never more CTA groups than can be co-resident (the
   // wave lockstep and the static unit schedule assume every group is live).
-  static int max_groups = 0;
-  if (max_groups == 0) {
-    TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Smem::kBytes));
-    lc.gridDim = dim3(num_sms());
-    int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0) {
-      cudaGetLastError();
-      active = num_sms() / CG;
+  // The smem attribute and the occupancy are per device: cached per device
+  // id (a process may drive several GPUs, or GPUs with other SM counts).
+  static std::mutex mu;
+  static int cached[kMaxDevices] = {};
+  int dev = 0;
+  TL_CUDA_TRY(cudaGetDevice(&dev));
+  TL_REQUIRE(dev >= 0 && dev < kMaxDevices, TL_ERR_UNSUPPORTED, "device %d", dev);
+  int max_groups;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cached[dev] == 0) {
+      TL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Smem::kBytes));
+      lc.gridDim = dim3(num_sms());
+      int active = 0;
+      if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0) {
+        cudaGetLastError();
+        active = num_sms() / CG;
+      }
+      cached[dev] = active < num_sms() / CG ? active : num_sms() / CG;
     }
-    max_groups = active < num_sms() / CG ? active : num_sms() / CG;
+    max_groups = cached[dev];
   }
   if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
   TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
@@ -207,21 +219,25 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t
 }
 
 
-// In place: fp16 logits z (written by the forward epilogue) -> bf16
-// dS = g (onehot(y) - p) - c p (z - E_p z), p = exp(z - lse).  One CTA per row.
-// dS for 8 logits held as fp16 in one 16-byte word:
-//   d = -g p - c p (z - E_p z) = p (A + B z),  A = c E_p z - g,  B = -c,
-//   p = 2^(z log2e - lse log2e)  (one FFMA + one SFU op per logit),
-// plus g at the target column (the one word that holds it).
-__device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float l2, float A, float B, int yy,
+// In place: fp16 u = (z - m) log2e (written by the forward epilogue, m =
+// the int16 offset of the 32-column slice, units of 1/128) -> bf16
+// dS = g (onehot(y) - p) - c p (z - E_p z).  With z = m + u ln2:
+//   p = 2^(u + K),  K = m log2e - lse log2e              (one FADD + one SFU op)
+//   dS = p (A' + B' u),  A' = c E_p z - g - c m,  B' = -c ln2   (one FFMA, one FMUL)
+// plus g at the target column (the one word that holds it).  K and A' are
+// per slice: one thread owns a whole slice (four 16-byte words), so the
+// offset is loaded and turned into (K, A') once per 32 logits.
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float K, float A, float B, int yy,
                                            float gg) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
   float d[8];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float2 z = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-    d[2 * k] = ex2_ftz(fmaf(z.x, kLog2e, -l2)) * fmaf(B, z.x, A);
-    d[2 * k + 1] = ex2_ftz(fmaf(z.y, kLog2e, -l2)) * fmaf(B, z.y, A);
+    const float2 u = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    d[2 * k] = ex2_ftz(u.x + K) * fmaf(B, u.x, A);
+    d[2 * k + 1] = ex2_ftz(u.y + K) * fmaf(B, u.y, A);
   }
   const int yl = yy - col0;
   if (static_cast<unsigned>(yl) < 8u) {
@@ -235,27 +251,78 @@ __device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float l2, float A,
 
 // Rows are grid-strided: one CTA per row when launched alone, or a small
 // persistent grid when it runs beside the next chunk's forward GEMM
-// (pipelined mode) and should trickle at low HBM intensity.  Two 16-byte
-// words in flight per thread (the pass is HBM-bound; in the step it runs at
-// the power-capped SM clock, so it is also kept short in instructions).
+// (pipelined mode) and should trickle at low HBM intensity.  A thread
+// streams one 32-logit slice (64 bytes: four 16-byte words in flight, read
+// through the non-coherent path so the warp's interleaved 16-byte requests
+// share L1 sectors) per step; the pass is HBM-bound and, at the power-capped
+// SM clock of the step, kept short in instructions.
+#ifndef TL_DS_VARIANT
+#define TL_DS_VARIANT 0
+#endif
 __global__ void __launch_bounds__(256)
-    dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec, int V, int rows,
+    dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec,
+                            const int16_t* __restrict__ zoff, long long ldo, int V, int rows,
                             const int32_t* __restrict__ y, const float* __restrict__ lse,
                             const float* __restrict__ g, const float* __restrict__ c,
                             const float* __restrict__ ez) {
+  const int nvec = (V + 7) / 8;
+  const int nsl = (nvec + 3) / 4;
+#if TL_DS_VARIANT == 3
+  __shared__ float s_off[8192];
+#endif
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r];
-    const float A = cc * ez[r] - gg, B = -cc;
+    const float A = cc * ez[r] - gg, B = -cc, Bu = -cc * kLn2;
     const int yy = y[r];
     uint4* row = buf + static_cast<long long>(r) * ld_vec;
-    const int nvec = (V + 7) / 8;
-    int v = threadIdx.x;
-    for (; v + static_cast<int>(blockDim.x) < nvec; v += 2 * blockDim.x) {
-      const uint4 q0 = row[v], q1 = row[v + blockDim.x];
-      row[v] = dsoftmax8(q0, v * 8, l2, A, B, yy, gg);
-      row[v + blockDim.x] = dsoftmax8(q1, (v + blockDim.x) * 8, l2, A, B, yy, gg);
+    const int16_t* off = zoff + static_cast<long long>(r) * ldo;
+#if TL_DS_VARIANT == 0 || TL_DS_VARIANT == 4
+    for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x) {
+      const float m = static_cast<float>(__ldg(off + sl)) * (1.f / 128.f);
+      const float K = fmaf(m, kLog2e, -l2), Aw = fmaf(B, m, A);
+      const int v0 = sl * 4;
+      if (v0 + 4 <= nvec) {
+        uint4 q[4];
+#if TL_DS_VARIANT == 0
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = __ldg(row + v0 + j);
+#else
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = row[v0 + j];
+#endif
+#pragma unroll
+        for (int j = 0; j < 4; ++j) row[v0 + j] = dsoftmax8(q[j], (v0 + j) * 8, K, Aw, Bu, yy, gg);
+      } else {
+        for (int v = v0; v < nvec; ++v) row[v] = dsoftmax8(row[v], v * 8, K, Aw, Bu, yy, gg);
+      }
     }
-    if (v < nvec) row[v] = dsoftmax8(row[v], v * 8, l2, A, B, yy, gg);
+#elif TL_DS_VARIANT == 1 || TL_DS_VARIANT == 2 || TL_DS_VARIANT == 3
+#if TL_DS_VARIANT == 3
+    __syncthreads();
+    for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x)
+      s_off[sl] = static_cast<float>(__ldg(off + sl)) * (1.f / 128.f);
+    __syncthreads();
+    auto word = [&](int v, uint4 q) {
+      const float m = s_off[v >> 2];
+      return dsoftmax8(q, v * 8, fmaf(m, kLog2e, -l2), fmaf(B, m, A), Bu, yy, gg);
+    };
+#else
+    auto word = [&](int v, uint4 q) {
+      const float m = static_cast<float>(__ldg(off + (v >> 2))) * (1.f / 128.f);
+      return dsoftmax8(q, v * 8, fmaf(m, kLog2e, -l2), fmaf(B, m, A), Bu, yy, gg);
+    };
+#endif
+    constexpr int kIn = TL_DS_VARIANT == 2 ? 4 : 2;
+    int v = threadIdx.x;
+    for (; v + (kIn - 1) * static_cast<int>(blockDim.x) < nvec; v += kIn * blockDim.x) {
+      uint4 q[kIn];
+#pragma unroll
+      for (int j = 0; j < kIn; ++j) q[j] = row[v + j * blockDim.x];
+#pragma unroll
+      for (int j = 0; j < kIn; ++j) row[v + j * blockDim.x] = word(v + j * blockDim.x, q[j]);
+    }
+    for (; v < nvec; v += blockDim.x) row[v] = word(v, row[v]);
+#endif
   }
 }
 
@@ -284,7 +351,7 @@ int grid_for(long long n, int block) {
 // --------------------------------------------------------------- workspace --
 struct ChunkWs {
   uint16_t* h;      // [C, H]
-  float4* part;     // [kMaxStripsFwd, C]
+  float4* part;     // [kStripsFwd, C]
   int32_t* y;       // [C]
   float* lse;       // [C]
   float* g;         // [C]
@@ -292,7 +359,8 @@ struct ChunkWs {
   float* ez;        // [C]
   float* logp;      // [C]
   float* ent;       // [C]
-  uint16_t* ds;     // [C, Vld]
+  uint16_t* ds;     // [C, Vld]  fp16 u = (z - m) log2e, then bf16 dS in place
+  int16_t* zoff;    // [C, ldo]  int16 slice offsets m of the fp16 u (store mode)
   // step-level
   float* term;      // [T]
   float* k3o;       // [T]
@@ -306,28 +374,34 @@ struct ChunkWs {
 
 constexpr int kSyncWaves = 4096;
 
-// Tuning overrides (profiling only).
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
+// Schedule parameters, measured at C2 on power-capped B200s (
+// the A/B runs that chose them are in the git history of tools/experiments).
+namespace tune {
+// L2 eviction priority of TMA operand loads / stores (make_policy kinds)
+constexpr int kNormal = 0, kEvictFirst = 1, kEvictLast = 2;
+// forward: h_c rows reused by every W tile of the strip (evict_last), W tiles
+// consumed within one lockstep window (evict_first): fwd -4.9 % (gpu_r51)
+constexpr int kFwdPolA = kEvictLast, kFwdPolB = kEvictFirst;
+constexpr int kFwdZStorePolicy = kEvictFirst;  // fp16 u stores: read once, by the dS pass
+// forward lockstep: steps of 4 tiles, window 1, per (M group, strip): 1 -> 2
+// -> 4-tile steps -0.5 / -0.4 %, 4 beats 8 by 0.3 % (gpu_r25, r30-r32, r57)
+constexpr int kFwdSyncTiles = 4, kFwdSyncWindow = 1, kFwdSyncSplit = 1;
+// dH / dW: dS streams (evict_first); W (dH) and h_c (dW) are re-read by every
+// wave (evict_last): dH -1.1 %, dW -2.8 % (gpu_r50)
+constexpr int kDhPolA = kEvictFirst, kDhPolB = kEvictLast;
+constexpr int kDwPolA = kEvictFirst, kDwPolB = kEvictLast;
+// dH / dW lockstep: 64-k-block steps, window 1 (without: step +7.8 %, gpu_r21)
+constexpr int kBwdSyncBlocks = 64, kBwdSyncWindow = 1;
+// pipelined mode: CTAs per SM of the dS pass running beside the forward
+constexpr int kDsOverlapCtasPerSm = 2;
+}  // namespace tune
 
-// Tuning overrides (profiling only): TL_SYNC_<name>=every,window ; every=0 disables.
-void sync_override(const char* name, int& every, int& window) {
-  char key[64];
-  snprintf(key, sizeof(key), "TL_SYNC_%s", name);
-  const char* v = getenv(key);
-  if (v) sscanf(v, "%d,%d", &every, &window);
-}
-
-// Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr).
-GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* name = nullptr,
-                    int split_dflt = 0) {
-  if (name) sync_override(name, every, window);
-  s.serpentine = env_int("TL_SERPENTINE", 1);
+// Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr) and
+// turn on the serpentine K order.
+GemmShape with_sync(GemmShape s, int* ctr, int every, int window, int split = 0) {
+  s.serpentine = 1;
   const int n_pairs = num_sms() / s.cg;
   const int waves = (s.n_units + n_pairs - 1) / n_pairs;
-  const int split = name ? env_int((std::string("TL_SYNC_SPLIT_") + name).c_str(), split_dflt) : 0;
   if (ctr && waves * (split ? 8 : 1) <= kSyncWaves && every > 0) {
     s.sync_ctr = ctr;
     s.sync_every = every;
@@ -338,12 +412,14 @@ GemmShape with_sync(GemmShape s, int* ctr, int every, int window, const char* na
 }
 
 long long vld_of(int vocab) { return (vocab + 7) / 8 * 8; }
+// int16 slice offsets per row: 8 per 256-column forward tile (16-byte stores)
+long long ldo_of(int vocab) { return (vocab + kBN - 1) / kBN * 8; }
 
 // Chunk buffers (h_c, partials, per-row stats, dS, lockstep counters) once,
 // or twice when `second` is given (pipelined mode); step-level buffers once.
 void carve_chunk(Workspace& w, ChunkWs& c, int C, int H, int V, bool with_bwd) {
   c.h = w.take<uint16_t>(static_cast<size_t>(C) * H);
-  c.part = w.take<float4>(static_cast<size_t>(kMaxStripsFwd) * C);
+  c.part = w.take<float4>(static_cast<size_t>(kStripsFwd) * C);
   c.y = w.take<int32_t>(C);
   c.lse = w.take<float>(C);
   c.g = w.take<float>(C);
@@ -352,6 +428,7 @@ void carve_chunk(Workspace& w, ChunkWs& c, int C, int H, int V, bool with_bwd) {
   c.logp = w.take<float>(C);
   c.ent = w.take<float>(C);
   c.ds = with_bwd ? w.take<uint16_t>(static_cast<size_t>(C) * vld_of(V)) : nullptr;
+  c.zoff = with_bwd ? w.take<int16_t>(static_cast<size_t>(C) * ldo_of(V)) : nullptr;
   c.sync = w.take<int>(5 * kSyncWaves);
   if (with_bwd) {
     c.tail_part = w.take<float>(static_cast<size_t>(kTailSlots) * kBM * kBNWide);
@@ -413,26 +490,24 @@ struct StreamPair {
 // forward depends on the lockstep more (none: +10.6 %) and 4 beats 8 by 0.3 %.
 GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
   const int n_tiles = (V + kBN - 1) / kBN;
-  int strips = env_int("TL_FWD_STRIPS", kStripsFwd);
-  strips = strips < 1 ? 1 : (strips > kMaxStripsFwd ? kMaxStripsFwd : strips);
-  const int strip = (n_tiles + strips - 1) / strips;
-  const int group_m = env_int("TL_FWD_GROUPM", num_sms() / kCG / 2);
-  // L2 priorities: the wave's h_c rows are re-read for every W tile of the
-  // strip (evict_last); a W tile is used by the strip's pairs within one
-  // lockstep window and not again this wave (evict_first): -4.9 % forward
-  // (tools/experiments/gpu_r51).
-  GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, env_int("TL_FWD_POLA", 2),
-                           env_int("TL_FWD_POLB", 1));
-  // per-strip lockstep: a strip's 37 pairs (sharing its W tiles) wait on each
+  const int strip = (n_tiles + kStripsFwd - 1) / kStripsFwd;
+  const int group_m = num_sms() / kCG / 2;  // a wave = 2 strips x (pairs / 2) M tiles
+  GemmShape s = make_shape(rows, V, H, kBN, strip, group_m, kCG, tune::kFwdPolA, tune::kFwdPolB);
+  // per-strip lockstep: a strip's pairs (sharing its W tiles) wait on each
   // other only, not on the other strip of the wave
-  return with_sync(s, sync, 4 * s.k_blocks, 1, "FWD", 1);
+  s = with_sync(s, sync, tune::kFwdSyncTiles * s.k_blocks, tune::kFwdSyncWindow,
+                tune::kFwdSyncSplit);
+  // K order by vocab tile: a row's logits (and logp / entropy / dS) are
+  // bitwise the same whatever chunk, M tile or rank it is processed in
+  s.serpentine = 2;
+  return s;
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
 // keep the chunk's logits in fp16 for the backward (store mode).
 int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int H, int V,
                          CombineArgs ca, cudaStream_t st, __half_raw* zout = nullptr,
-                         long long ldz = 0) {
+                         long long ldz = 0, int16_t* zoff = nullptr) {
   CUtensorMap ma, mb;
   if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
   // fresh wave-lockstep counters for this chunk's GEMMs (fwd / dS / dH / dW)
@@ -443,8 +518,8 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
-  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, c.sync + 4 * kSyncWaves, ca,
-                         env_int("TL_Z_POLICY", 1)};
+  EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, zoff, ldo_of(V), c.sync + 4 * kSyncWaves, ca,
+                         tune::kFwdZStorePolicy};
   return launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD);
 }
 
@@ -478,7 +553,7 @@ extern "C" size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hid
   Workspace w{nullptr, 0};
   ChunkWs second{};
   carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true,
-        (mode & ~TL_LMHEAD_ACCUMULATE_DW) == TL_LMHEAD_STORE_LOGITS_PIPELINED ? &second : nullptr);
+        (mode & 0xFF) == TL_LMHEAD_STORE_LOGITS_PIPELINED ? &second : nullptr);
   return w.used + 1024;
 }
 
@@ -497,7 +572,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   const int sel = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
   if (c_fp32 && N >= 1024) {  // wide 256 x 512 pair tiles (as the dH / dW GEMMs)
     const GemmShape s = make_shape(M, N, K, kBNWide, 1, kGroupM, kCG);
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0, 0};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32, kBNWide>(ma, mb, s, ep, st);
@@ -507,7 +582,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
   }
   const GemmShape s = make_shape(M, N, K, kBN, 1, kGroupM, kCG);
   if (c_fp32) {
-    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate, 0, 0};
+    EpiStoreF32::Params ep{static_cast<float*>(C), ldc, accumulate};
     switch (sel) {
       case 0: return launch_gemm<kCG, false, false, EpiStoreF32>(ma, mb, s, ep, st);
       case 1: return launch_gemm<kCG, false, true, EpiStoreF32>(ma, mb, s, ep, st);
@@ -516,7 +591,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
     }
   }
   TL_REQUIRE(!accumulate, TL_ERR_UNSUPPORTED, "accumulate needs fp32 C");
-  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr, 0};
+  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr};
   switch (sel) {
     case 0: return launch_gemm<kCG, false, false, EpiStoreBF16>(ma, mb, s, ep, st);
     case 1: return launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st);
@@ -567,8 +642,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                    double* report, int32_t chunk_rows, int32_t mode_flags,
                                    void* workspace, size_t workspace_bytes, tl_stream_t stream) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
-  const int mode = mode_flags & ~TL_LMHEAD_ACCUMULATE_DW;
+  const int mode = mode_flags & ~(TL_LMHEAD_ACCUMULATE_DW | TL_LMHEAD_NO_SPLIT_TAIL);
   const bool acc_dw = (mode_flags & TL_LMHEAD_ACCUMULATE_DW) != 0;
+  const bool no_split_tail = (mode_flags & TL_LMHEAD_NO_SPLIT_TAIL) != 0;
   TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE ||
                  mode == TL_LMHEAD_STORE_LOGITS_PIPELINED,
              TL_ERR_INVALID_ARG, "unknown lmhead mode %d", mode_flags);
@@ -587,7 +663,10 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "lmhead workspace too small (%zu < %zu)", workspace_bytes,
              w.used);
   const long long Vld = vld_of(V);
-  const float ent_grad = n_act > 0 ? static_cast<float>(-cfg->entropy_coef / double(n_act)) : 0.f;
+  // dLoss/dentropy per action token: the bonus is a mean over the step's
+  // global action tokens (entropy_norm), not this micro-batch's / rank's
+  const double ent_norm = cfg->entropy_norm > 0 ? cfg->entropy_norm : double(n_act);
+  const float ent_grad = n_act > 0 ? static_cast<float>(-cfg->entropy_coef / ent_norm) : 0.f;
 
   // observation rows: zero their term state and (if training) their dH rows
   if (n_tokens > 0) {
@@ -650,7 +729,8 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     ca.ez_row = b.ez;
     ca.lse_row = b.lse;
     return lmhead_forward_chunk(b, weight, rows, H, V, ca, st,
-                                store ? reinterpret_cast<__half_raw*>(b.ds) : nullptr, Vld);
+                                store ? reinterpret_cast<__half_raw*>(b.ds) : nullptr, Vld,
+                                store ? b.zoff : nullptr);
   };
   // stage S: dS for the chunk (in place over its fp16 logits, or recomputed)
   auto stage_ds = [&](long long i, cudaStream_t s_ds, int grid) -> int {
@@ -659,7 +739,8 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     if (store) {
       ProfScope prof(PROF_DSOFTMAX, s_ds);
       dsoftmax_inplace_kernel<<<grid < rows ? grid : rows, 256, 0, s_ds>>>(
-          reinterpret_cast<uint4*>(b.ds), Vld / 8, V, rows, b.y, b.lse, b.g, b.c, b.ez);
+          reinterpret_cast<uint4*>(b.ds), Vld / 8, b.zoff, ldo_of(V), V, rows, b.y, b.lse, b.g,
+          b.c, b.ez);
       TL_LAUNCH_CHECK();
       count_launch();
       return TL_OK;
@@ -685,28 +766,25 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       // dS streams (evict_first); W is re-read by every wave and the
       // serpentine order starts each wave on what the last one read
       // (evict_last): -1.1 % dH (gpu_r50)
-      const GemmShape sh = with_sync(make_shape(rows, H, V, kBNWide, 1, 1, kCG,
-                                                env_int("TL_DH_POLA", 1), env_int("TL_DH_POLB", 2)),
-                                     b.sync + 2 * kSyncWaves, 64, 1, "DH");
+      const GemmShape sh = with_sync(
+          make_shape(rows, H, V, kBNWide, 1, 1, kCG, tune::kDhPolA, tune::kDhPolB),
+          b.sync + 2 * kSyncWaves, tune::kBwdSyncBlocks, tune::kBwdSyncWindow);
       // dhidden rows are written once and not read again in the step
-      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci,
-                              env_int("TL_DH_OUT_POLICY", 0)};
+      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
         return e;
     }
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
-    // dS streams (evict_first), h_c is re-read by every wave (evict_last): -2.8 % dW
-    GemmShape sh = with_sync(make_shape(V, H, rows, kBNWide, 1, 1, kCG, env_int("TL_DW_POLA", 1),
-                                        env_int("TL_DW_POLB", 2)),
-                             b.sync + 3 * kSyncWaves, 64, 1, "DW");
-    if (env_int("TL_DW_TAIL", 1)) {  // split-K tail for the partial last wave
+    GemmShape sh = with_sync(
+        make_shape(V, H, rows, kBNWide, 1, 1, kCG, tune::kDwPolA, tune::kDwPolB),
+        b.sync + 3 * kSyncWaves, tune::kBwdSyncBlocks, tune::kBwdSyncWindow);
+    if (!no_split_tail) {  // split-K tail for the partial last wave
       sh.tail_part = b.tail_part;
       sh.tail_ctr = b.tail_ctr;
     }
-    EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0, env_int("TL_DW_LOAD_ADD", 0),
-                           env_int("TL_DW_OUT_POLICY", 0)};
+    EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
   };
 
@@ -725,7 +803,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     // first and the pass (a small grid-strided grid) fills the remaining slots.
     StreamPair sp;
     if (sp.err) return sp.err;
-    const int ds_grid = env_int("TL_DS_OVERLAP_CTAS", 2) * num_sms();
+    const int ds_grid = tune::kDsOverlapCtasPerSm * num_sms();
     if (int e = stage_fwd(0)) return e;
     for (long long i = 0; i < n_chunks; ++i) {
       TL_CUDA_TRY(cudaEventRecord(sp.ev_fwd, st));  // F_i done

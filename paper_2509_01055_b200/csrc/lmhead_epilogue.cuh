@@ -24,30 +24,6 @@ __device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
   return r;
 }
 
-// 32 consecutive fp32 accumulator columns -> fp16 (saturating), 4 x 16-byte stores.
-// The stores carry an L2 eviction hint (`pol`): the chunk's logits are only
-// read back by the next kernel, so they should not push the wave's resident
-// h_c rows out of L2.
-__device__ __forceinline__ void store_f16_row(__half_raw* dst, const uint32_t (&r)[32], int nvalid,
-                                              uint64_t pol) {
-  if (nvalid >= 32) {
-#pragma unroll
-    for (int j = 0; j < 32; j += 8) {
-      uint4 v;
-      v.x = pack_f16x2_sat(__uint_as_float(r[j + 0]), __uint_as_float(r[j + 1]));
-      v.y = pack_f16x2_sat(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-      v.z = pack_f16x2_sat(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
-      v.w = pack_f16x2_sat(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
-      st_v4_hint(dst + j, v, pol);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)  // static indexing keeps r[] in registers
-      if (j < nvalid)
-        dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(__uint_as_float(r[j]), 0.f) & 0xFFFFu);
-  }
-}
-
 struct CombineArgs {
   const float4* part;
   int n_strips, rows;
@@ -123,22 +99,42 @@ __device__ void combine_row(const CombineArgs& a, int r) {
 }
 
 // Online log-sum-exp over a vocab strip; one thread = one token row.
+//
+// Backward input (store mode): instead of the logits themselves, the
+// epilogue keeps u = (z - m) log2e in fp16, where m is the row's running
+// max, rounded UP to a multiple of 1/128, after the 32-column slice that
+// holds z.  u <= 0 always, and the dS pass recovers p = 2^(u + (m - lse)
+// log2e) and z = m + u ln2 with m read back exactly from a per-(row, slice)
+// int16 offset (units of 1/128).  An fp16 error in u costs p an absolute
+// error <= p |u| 2^-11 <= 2^-11 / e, and the row's top token sits within
+// 1/128 of its offset (u > -0.012: fp16 spacing <= 2^-17), so the
+// high-probability tokens, whose p cancels against onehot(y) in dS, keep
+// ~fp32 precision.  Storing z in fp16 directly cost them up to 2^-7
+// relative at |z| >= 16 (per-row dH errors up to 6.6x on p_y -> 1 rows,
+// tests/test_lmhead_bwd_fullshape_gpu.py).  The quantised m also drives the
+// log-sum-exp itself (any offset >= the max works).
+constexpr float kOffScale = 128.f;             // offset units: 1/128
+constexpr float kMaxOff = 32767.f / kOffScale;  // |m| cap (|z| beyond ~256: unsupported)
+
 struct EpiLseStats {
   static constexpr bool kSplitTail = false;
   struct Params {
     const int32_t* targets;  // [C] target id of each chunk row
     float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
     int rows;                // C (partials row stride)
-    __half_raw* zout;        // optional fp16 logit tile store [C, ldz] (backward input)
+    __half_raw* zout;        // optional fp16 u = (z - m) log2e store [C, ldz] (backward input)
     long long ldz;
+    int16_t* zoff;           // [C, ldo] slice offsets m (8 per 256-column tile), with zout
+    long long ldo;
     int* tile_ctr;           // [ceil(C/128)] strips finished per 128-row block (zeroed)
     CombineArgs ca;          // last-strip fixup: merge + surrogate for the block's rows
-    int z_policy;            // make_policy() kind of the fp16 logit stores
+    int z_policy;            // make_policy() kind of the fp16 stores
   };
   struct State {
     float m, s, t, zy;
     int y;
     uint64_t zpol;
+    uint64_t olo, ohi;  // the tile's 8 slice offsets (int16), shifted in slice by slice
   };
   __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
                                     const UnitCoord&) {
@@ -148,17 +144,16 @@ struct EpiLseStats {
     st.zy = -INFINITY;
     st.y = row < sh.M ? p.targets[row] : -1;
     st.zpol = make_policy(p.z_policy);
+    st.olo = st.ohi = 0;
   }
-  // One 32-column slice of the row: fp16 store, running max rescale, then
-  // sum e and sum e*z with e = 2^(z*log2e - m*log2e).  Full slices (all but
-  // the vocab tail) take a branch-free path: 3-input max, one SFU op per
-  // logit, split accumulators; the target column is looked up only in the
-  // one slice that holds it.
+  // One 32-column slice of the row: running max rescale, then sum e and
+  // sum e*z with e = 2^u, u = z*log2e - m*log2e, and (store mode) fp16 u.
+  // Full slices (all but the vocab tail) take a branch-free path: 3-input
+  // max, one SFU op per logit, split accumulators; the target column is
+  // looked up only in the one slice that holds it.
   __device__ static __forceinline__ void slice(const Params& p, const GemmShape& sh, State& st,
                                                int row, int cb, const uint32_t (&r)[32]) {
     const int nvalid = sh.N - cb;  // columns >= N are padding
-    if (p.zout && row < sh.M)
-      store_f16_row(p.zout + static_cast<long long>(row) * p.ldz + cb, r, nvalid, st.zpol);
     const int yl = st.y - cb;
     if (static_cast<unsigned>(yl) < 32u) {
 #pragma unroll
@@ -181,41 +176,62 @@ struct EpiLseStats {
         if (j < nvalid) cm = fmaxf(cm, __uint_as_float(r[j]));
     }
     if (cm > st.m) {
-      const float f = ex2_ftz((st.m - cm) * kLog2e);
+      const float mq = fminf(ceilf(cm * kOffScale) * (1.f / kOffScale), kMaxOff);
+      const float f = ex2_ftz((st.m - mq) * kLog2e);
       st.s *= f;
       st.t *= f;
-      st.m = cm;
+      st.m = mq;
     }
     const float mb = st.m * kLog2e;
+    const bool keep = p.zout != nullptr && row < sh.M;
+    __half_raw* dst = keep ? p.zout + static_cast<long long>(row) * p.ldz + cb : nullptr;
     float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
     if (nvalid >= 32) {
+      uint32_t hq[16];
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
         const float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
-        const float e0 = ex2_ftz(fmaf(v0, kLog2e, -mb)), e1 = ex2_ftz(fmaf(v1, kLog2e, -mb));
+        const float u0 = fmaf(v0, kLog2e, -mb), u1 = fmaf(v1, kLog2e, -mb);
+        const float e0 = ex2_ftz(u0), e1 = ex2_ftz(u1);
         s0 += e0;
         s1 += e1;
         t0 = fmaf(e0, v0, t0);
         t1 = fmaf(e1, v1, t1);
+        hq[j / 2] = pack_f16x2_sat(u0, u1);
+      }
+      if (keep) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_v4_hint(dst + 8 * q, make_uint4(hq[4 * q], hq[4 * q + 1], hq[4 * q + 2], hq[4 * q + 3]),
+                     st.zpol);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float v = __uint_as_float(r[j]);
-        const float e = j < nvalid ? ex2_ftz(fmaf(v, kLog2e, -mb)) : 0.f;
+        const float u = fmaf(v, kLog2e, -mb);
+        const float e = j < nvalid ? ex2_ftz(u) : 0.f;
         s0 += e;
         t0 = fmaf(e, v, t0);
+        if (keep && j < nvalid)
+          dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(u, 0.f) & 0xFFFFu);
       }
     }
     st.s += s0 + s1;
     st.t += t0 + t1;
+    if (p.zout) {  // this slice's offset m into the tile's 8-slot shift register
+      const uint64_t m16 =
+          static_cast<uint16_t>(static_cast<int16_t>(fmaxf(st.m, -kMaxOff) * kOffScale));
+      st.olo = (st.olo >> 16) | (st.ohi << 48);
+      st.ohi = (st.ohi >> 16) | (m16 << 48);
+    }
   }
   // TMEM loads are double-buffered: slice c+1 is in flight while slice c is
   // reduced (tcgen05.wait::ld waits for all outstanding loads).
   template <int BN>
   __device__ static void tile(const Params& p, const GemmShape& sh, State& st, int row, int col0,
                               uint32_t taddr) {
-    static_assert(BN % 64 == 0, "slices are processed in pairs");
+    static_assert(BN == 256, "slice offsets are stored 8 (16 bytes) per 256-column tile");
     uint32_t ra[32], rb[32];
     tmem_ld32(taddr, ra);
     tmem_ld_wait_regs(ra);
@@ -229,6 +245,11 @@ struct EpiLseStats {
       slice(p, sh, st, row, col0 + c + 32, rb);
       if (more) tmem_ld_wait_regs(ra);
     }
+    if (p.zout && row < sh.M)
+      st_v4_hint(p.zoff + static_cast<long long>(row) * p.ldo + col0 / 32,
+                 make_uint4(static_cast<uint32_t>(st.olo), static_cast<uint32_t>(st.olo >> 32),
+                            static_cast<uint32_t>(st.ohi), static_cast<uint32_t>(st.ohi >> 32)),
+                 st.zpol);
   }
   // Publish this strip's row stats; the CTA that finishes the LAST strip of a
   // 128-row block (stream-K style fixup, counter per block) merges all strips

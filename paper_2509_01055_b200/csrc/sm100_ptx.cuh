@@ -119,12 +119,6 @@ __device__ __forceinline__ void red_add_v4_f32(float* p, float4 v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
-// ... with an L2 eviction-priority hint on the reduced line.
-__device__ __forceinline__ void red_add_v4_f32_hint(float* p, float4 v, uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
 // 16-byte store with an L2 eviction-priority hint (createpolicy).
 __device__ __forceinline__ void st_v4_hint(void* p, uint4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),

@@ -114,7 +114,7 @@ class GRPOStep:
 
     def __init__(self, hidden_dim: int, vocab: int, cfg: LossConfig | None = None,
                  chunk_rows: int | None = None, recompute: bool = False,
-                 pipelined: bool = False):
+                 pipelined: bool = False, split_tail: bool = True):
         """recompute=False keeps each chunk's logits in fp16 for the backward
         (6*T*H*V FLOPs); True recomputes them in a second GEMM (8*T*H*V) so no
         logit ever leaves TMEM.  pipelined=True (store mode) double-buffers the
@@ -133,6 +133,8 @@ class GRPOStep:
             self.mode = _lib.LMHEAD_STORE_LOGITS_PIPELINED
         else:
             self.mode = _lib.LMHEAD_STORE_LOGITS
+        # split_tail=False (tests): the dW GEMM's partial last wave runs unsplit
+        self.flags = 0 if split_tail else _lib.LMHEAD_NO_SPLIT_TAIL
         self._ws = _Workspace()
         self.last_chunk = None  # chunk rows used by the latest call
 
@@ -268,7 +270,9 @@ class GRPOStep:
         ws_bytes = int(L.tl_lmhead_step_workspace_bytes(chunk, self.H, self.V, T, packed.n_traj,
                                                         n_groups, self.mode))
         plan.ws = self._ws.get(ws_bytes, dev)
-        plan.cfg_c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0)
+        plan.cfg_c = cfg.to_c(use_mask=1, has_ref=int(logp_ref is not None), objective=0,
+                              entropy_norm=float(norm_tokens if norm_tokens is not None
+                                                 else max(packed.n_act, 1)))
         plan.keep = (packed, hidden, weight, logp_old, logp_ref)  # pointers stay valid
         plan.step_args = (
             hidden.data_ptr(), weight.data_ptr(), packed.input_ids.data_ptr(),
@@ -278,7 +282,7 @@ class GRPOStep:
             plan.traj_w.data_ptr(), T, self.H, self.V, packed.n_traj, n_groups, plan.cfg_c,
             plan.logp.data_ptr(), plan.ent.data_ptr(), _lib.ptr(plan.dh), _lib.ptr(plan.dw),
             plan.rep.data_ptr(), chunk,
-            self.mode | (_lib.LMHEAD_ACCUMULATE_DW if accumulate_dweight else 0),
+            self.mode | self.flags | (_lib.LMHEAD_ACCUMULATE_DW if accumulate_dweight else 0),
             plan.ws.data_ptr(), ws_bytes)
         return plan
 

@@ -8,7 +8,13 @@ the group's action-token count, the LM head's work), every rank runs the
 fused step on its shard with the GLOBAL normalisers (n_groups, action
 tokens), and the only collectives are
   N1  all-reduce of the report's additive partials (~12 doubles), and
-  N2  all-reduce of dW (the LM-head weight gradient) when it is trained.
+  N2  all-reduce of dW (the LM-head weight gradient) when it is trained, or
+      its reduce-scatter into row shards when W is partitioned.
+They run at the C ABI over the library's own NCCL communicator
+(`NcclComm`, tl_nccl_* / tl_allreduce_* in include/toolloop_b200.h),
+stream-ordered after the step on the caller's stream.  `allreduce_report` /
+`allreduce_grad` are the same reductions through torch.distributed, for
+process groups NCCL cannot serve (gloo: several ranks on one GPU, CPU tests).
 """
 
 from __future__ import annotations
@@ -85,3 +91,97 @@ def allreduce_grad(t, group=None):
 
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
+
+
+class NcclComm:
+    """An NCCL communicator owned by the C library (tl_nccl_comm_init), for
+    the step's N1 / N2 collectives at the C ABI.  Build it collectively:
+    rank 0 draws the unique id (tl_nccl_unique_id) and the existing
+    torch.distributed group broadcasts it (`from_process_group`)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        import ctypes
+
+        from . import _lib
+
+        L = _lib.lib()
+        if not L.tl_nccl_available():
+            from .errors import ToolloopError
+
+            raise ToolloopError("NCCL (libnccl.so.2) is not loadable")
+        buf = ctypes.create_string_buffer(bytes(unique_id), _lib.TL_NCCL_UNIQUE_ID_BYTES)
+        h = ctypes.c_void_p()
+        _lib.check(L.tl_nccl_comm_init(ctypes.byref(h), ctypes.addressof(buf), nranks, rank))
+        self.handle = h.value
+        self.nranks = nranks
+        self.rank = rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _lib
+
+        buf = ctypes.create_string_buffer(_lib.TL_NCCL_UNIQUE_ID_BYTES)
+        _lib.check(_lib.lib().tl_nccl_unique_id(ctypes.addressof(buf)))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "NcclComm":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world, rank)
+
+    def size(self) -> int:
+        import ctypes
+
+        from . import _lib
+
+        n = ctypes.c_int32()
+        _lib.check(_lib.lib().tl_nccl_comm_size(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+    def allreduce_report(self, rep_tensor, agg: int = 0, stream=None):
+        """N1 at the C ABI: the float64 [TL_REPORT_LEN] device report of this
+        rank -> the global report, in place, stream-ordered."""
+        from . import _lib
+
+        _lib.check(_lib.lib().tl_allreduce_report(self.handle, rep_tensor.data_ptr(), agg,
+                                                  _lib.stream_handle(stream)))
+        return rep_tensor
+
+    def allreduce_scalars(self, x, stream=None):
+        from . import _lib
+
+        _lib.check(_lib.lib().tl_allreduce_scalars(self.handle, x.data_ptr(), x.numel(),
+                                                   _lib.stream_handle(stream)))
+        return x
+
+    def allreduce_grad(self, t, stream=None):
+        """N2 at the C ABI: fp32 gradient summed over ranks, in place."""
+        from . import _lib
+
+        _lib.check(_lib.lib().tl_allreduce_f32(self.handle, t.data_ptr(), t.numel(),
+                                               _lib.stream_handle(stream)))
+        return t
+
+    def reduce_scatter_grad(self, t, shard, stream=None):
+        """N2 for a row-partitioned W: shard (numel = t.numel() / nranks)
+        receives this rank's rows of the summed gradient."""
+        from . import _lib
+
+        if shard.numel() * self.nranks != t.numel():
+            raise ValueError("shard must hold numel / nranks elements")
+        _lib.check(_lib.lib().tl_reduce_scatter_f32(self.handle, t.data_ptr(), shard.data_ptr(),
+                                                    shard.numel(), _lib.stream_handle(stream)))
+        return shard
+
+    def close(self) -> None:
+        if self.handle:
+            from . import _lib
+
+            _lib.check(_lib.lib().tl_nccl_comm_destroy(self.handle))
+            self.handle = None

@@ -81,13 +81,14 @@ class LossConfig:
         if self.loss_agg not in (AGG_REFERENCE, AGG_TOKEN_MEAN):
             raise ValueError(f"loss_agg must be {AGG_REFERENCE!r} or {AGG_TOKEN_MEAN!r}")
 
-    def to_c(self, *, use_mask: int = 1, has_ref: int = 0, objective: int = 0) -> _lib.LossConfigC:
+    def to_c(self, *, use_mask: int = 1, has_ref: int = 0, objective: int = 0,
+             entropy_norm: float = 0.0) -> _lib.LossConfigC:
         return _lib.LossConfigC(
             eps_low=self.epsilon_clip,
             eps_high=self.epsilon_clip if self.eps_high is None else self.eps_high,
             kl_beta=self.kl_beta, entropy_coef=self.entropy_coef, use_mask=use_mask,
             has_ref=has_ref, objective=objective,
-            agg=1 if self.loss_agg == AGG_TOKEN_MEAN else 0)
+            agg=1 if self.loss_agg == AGG_TOKEN_MEAN else 0, entropy_norm=float(entropy_norm))
 
 
 @dataclass

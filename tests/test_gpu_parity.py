@@ -634,8 +634,6 @@ def test_dw_split_k_tail_vs_oracle():
     idle pairs and the last slice to arrive sums them in order.  Checked
     against the oracle backward across several chunks (store and accumulate
     epilogues), bitwise run to run, and against the unsplit kernel."""
-    import os
-
     from oracle import lmhead_oracle as LH
 
     H, V = 3584, 3072
@@ -656,11 +654,8 @@ def test_dw_split_k_tail_vs_oracle():
     dw1 = r1.dweight.clone()
     r2 = step(packed, go, rewards, h, W, f(lold), f(lref))
     assert torch.equal(dw1, r2.dweight)
-    os.environ["TL_DW_TAIL"] = "0"
-    try:
-        r3 = step(packed, go, rewards, h, W, f(lold), f(lref))
-    finally:
-        del os.environ["TL_DW_TAIL"]
+    r3 = grpo.GRPOStep(H, V, cfg, chunk_rows=512, split_tail=False)(
+        packed, go, rewards, h, W, f(lold), f(lref))
     assert _rel_fro(dw1.cpu().numpy(), r3.dweight.cpu().numpy()) <= 1e-6
     # oracle
     ids = packed.input_ids.cpu().numpy()

@@ -1,0 +1,179 @@
+"""LM-head backward (dH / dW) parity at the benched shapes.
+
+The fused GRPO step at the C2 (H 3584, V 152064) and C5 (H 4096, V 151936)
+LM-head shapes, one whole synthetic group of the config (C2: ~17 k action
+rows, C5: ~40 k, so several chunks, 6 vocab strips, lockstep waves and the
+dW split-K tail at its real size), against the float64 restatement
+`oracle.lmhead_oracle.lmhead_fwd_bwd_f64` on the same bf16 inputs.  The
+upstream per-token gradients come from the oracle's own forward (logp) and
+the clipped-surrogate restatement (oracle.grpo_oracle.term_and_grad), so the
+GPU forward, the fused surrogate epilogue, the dS pass and the dH / dW GEMMs
+are all checked.
+
+Two logit scales:
+  init       W ~ N(0, 0.02): logit std ~1.2 (the bench's synthetic weights)
+  realistic  W std so that max |z| ~ 30 (trained LM heads reach |z| 20-40),
+             and half the action rows target their arg-max token (p_y -> 1),
+             where an imprecise p cancels against onehot(y) in dS.
+
+Tolerances (relative Frobenius vs the float64 oracle; the dominant error is
+dS rounded to bf16, 2^-9 relative per element, and dH's bf16 output):
+  dH 5e-3, dW 5e-3; logp / entropy abs 1e-4 + 1e-5 max|z| (the tensor
+  cores accumulate the logits in fp32: their error grows with |z|).
+Measured values are written to gpurun_out/bwd_parity.jsonl and quoted in
+DESIGN.md §4.
+"""
+
+import json
+import math
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import grpo_oracle as O
+from oracle import lmhead_oracle as LH
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2509_01055_b200 import grpo, packing  # noqa: E402
+from paper_2509_01055_b200.rl import loss as L  # noqa: E402
+from paper_2509_01055_b200.synthetic import CONFIGS, make_workload  # noqa: E402
+
+OUT = Path(os.environ.get("GRAFT_REPO_ROOT", Path(__file__).resolve().parents[1])) / "gpurun_out"
+
+DH_TOL = 5e-3
+DW_TOL = 5e-3
+
+
+def _rel_fro(a, b):
+    return float(torch.linalg.norm((a - b).flatten()) / max(float(torch.linalg.norm(b.flatten())), 1e-300))
+
+
+def _record(row):
+    OUT.mkdir(exist_ok=True)
+    with open(OUT / "bwd_parity.jsonl", "a") as f:
+        f.write(json.dumps(row) + "\n")
+    print(json.dumps(row))
+
+
+def _case(shape, scale, seed=0):
+    cfg = CONFIGS[shape]
+    H, V = cfg.hidden, cfg.vocab
+    wl = make_workload(cfg, group_ids=np.arange(1))
+    packed = packing.pack_table(wl.table)
+    T = packed.n_tokens
+    act = packed.act_idx.long()
+    g = torch.Generator(device="cuda").manual_seed(2509 + seed)
+    h = torch.randn((T, H), device="cuda", generator=g).bfloat16()
+    sw = 0.02 if scale == "init" else 30.0 / (4.4 * math.sqrt(H))
+    W = (torch.randn((V, H), device="cuda", generator=g) * sw).bfloat16()
+    if scale == "realistic":
+        # half the action rows target their arg-max token (confident tokens)
+        ids = packed.input_ids.clone()
+        sel = act[::2]
+        for s in range(0, sel.numel(), 8192):
+            rows = sel[s:s + 8192]
+            z = h[rows].float() @ W.float().T
+            ids[rows] = z.argmax(1).to(torch.int32)
+        packed.input_ids = ids
+    return cfg, wl, packed, h, W
+
+
+@pytest.mark.parametrize("mode", ["store", "recompute"])
+@pytest.mark.parametrize("scale", ["init", "realistic"])
+@pytest.mark.parametrize("shape", ["c2", "c5"])
+def test_backward_full_shape_vs_oracle(shape, scale, mode):
+    cfg, wl, packed, h, W = _case(shape, scale)
+    H, V = cfg.hidden, cfg.vocab
+    T, n_act = packed.n_tokens, packed.n_act
+    act = packed.act_idx.long()
+    ids_act = packed.input_ids.long()[act]
+    tot = packed.traj_of_token.cpu().numpy()
+    act_np = act.cpu().numpy()
+    go = wl.group_off
+    n_groups = len(go) - 1
+    token_mean = cfg.loss_agg == L.AGG_TOKEN_MEAN
+    beta, coef = 0.04, 0.01
+    lc = L.LossConfig(epsilon_clip=0.2, kl_beta=beta, entropy_coef=coef, loss_agg=cfg.loss_agg)
+
+    # behaviour / reference policy log-probs near the oracle's current logp
+    # (ratios ~ exp(N(0, 0.03)): no token sits on a clip boundary)
+    z_lp = _oracle_logp(h[act], W, ids_act)
+    rng = np.random.default_rng(11)
+    lold = np.asarray(wl.logp_old, dtype=np.float32).copy()
+    lref = np.asarray(wl.logp_ref, dtype=np.float32).copy()
+    lold[act_np] = (z_lp + rng.normal(0, 0.03, n_act)).astype(np.float32)
+    lref[act_np] = (lold[act_np] + rng.normal(0, 0.05, n_act)).astype(np.float32)
+    lold_t = torch.from_numpy(lold).cuda()
+    lref_t = torch.from_numpy(lref).cuda()
+
+    step = grpo.GRPOStep(H, V, lc, recompute=mode == "recompute")
+    res = step(packed, go, wl.rewards, h, W, lold_t, lref_t)
+    torch.cuda.synchronize()
+
+    # oracle upstream gradient per action row: -d term / d logp * traj weight
+    adv = np.zeros(packed.n_traj)
+    for gi in range(n_groups):
+        adv[go[gi]:go[gi + 1]] = O.group_advantages(wl.rewards[go[gi]:go[gi + 1]].tolist())
+    cu = packed.cu_seqlens.cpu().numpy()
+    ao = packed.act_off.cpu().numpy()
+    n_i = np.diff(ao)
+    G = np.diff(go)
+    gsize = np.repeat(G, G)
+    lo64 = lold.astype(np.float64)
+    lr64 = lref.astype(np.float64)
+
+    def g_fn(logp):
+        lp = logp.cpu().numpy()
+        out = np.empty(n_act)
+        for k in range(n_act):
+            p = act_np[k]
+            b = tot[p]
+            _, gr = O.term_and_grad(lp[k], lo64[p], lr64[p], adv[b], 0.2, beta)
+            w = 1.0 / n_act if token_mean else 1.0 / (n_i[b] * gsize[b] * n_groups)
+            out[k] = -gr * w
+        return torch.from_numpy(out)
+
+    logp, ent, lse, dH, dW = LH.lmhead_fwd_bwd_f64(h[act], W, ids_act, g_fn, -coef / n_act)
+    got_lp = res.logp[act].double()
+    got_en = res.entropy[act].double()
+    got_dh = res.dhidden[act].double()
+    got_dw = res.dweight.double()
+    e_lp = float((got_lp - logp).abs().max())
+    e_en = float((got_en - ent).abs().max())
+    e_dh = _rel_fro(got_dh, dH)
+    e_dw = _rel_fro(got_dw, dW)
+    # per-row dH errors (rows with a non-negligible gradient)
+    rn = torch.linalg.norm(dH, dim=1)
+    big = rn > 1e-3 * rn.max()
+    row_err = (torch.linalg.norm(got_dh - dH, dim=1)[big] / rn[big])
+    row = {"test": "bwd_full_shape", "shape": shape, "scale": scale, "mode": mode,
+           "H": H, "V": V, "n_act": n_act, "chunk_rows": step.last_chunk,
+           "max_abs_z": float(lse.max()), "p_y_max": float(torch.exp(logp).max()),
+           "logp_max_abs_err": e_lp, "ent_max_abs_err": e_en,
+           "dH_rel_fro": e_dh, "dW_rel_fro": e_dw,
+           "dH_max_abs_rel": float((got_dh - dH).abs().max() / dH.abs().max()),
+           "dW_max_abs_rel": float((got_dw - dW).abs().max() / dW.abs().max()),
+           "dH_row_rel_p50": float(row_err.median()), "dH_row_rel_p99": float(row_err.quantile(0.99)),
+           "dH_row_rel_max": float(row_err.max())}
+    _record(row)
+    assert torch.all(res.dhidden[packed.loss_mask == 0] == 0)
+    tol = 1e-4 + 1e-5 * float(lse.abs().max())
+    assert e_lp <= tol and e_en <= tol, row
+    assert e_dh <= DH_TOL, row
+    assert e_dw <= DW_TOL, row
+
+
+def _oracle_logp(h, W, y, chunk=4096):
+    out = []
+    W64 = W.double()
+    for s in range(0, h.shape[0], chunk):
+        z = h[s:s + chunk].double() @ W64.T
+        out.append((z.gather(1, y[s:s + chunk, None])[:, 0] - torch.logsumexp(z, 1)))
+    return torch.cat(out).cpu().numpy()
