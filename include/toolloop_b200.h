@@ -28,7 +28,8 @@
 extern "C" {
 #endif
 
-#define TL_ABI_VERSION 2  /* 2: tl_loss_config.entropy_norm, NCCL collectives */
+#define TL_ABI_VERSION 3  /* 2: tl_loss_config.entropy_norm, NCCL collectives
+                             3: tl_pack_varlen traj_drop, dW-only / dH-only steps */
 
 typedef void* tl_stream_t; /* cudaStream_t */
 
@@ -67,14 +68,20 @@ const char* tl_profile_category(int32_t i);
  * token ids stored at token_pool[seg_src_off[s] ...] (any order in the pool,
  * e.g. the arrival order of asynchronous rollout turns) and seg_is_action[s]
  * = 1 for Segment.origin == "action".
+ * traj_drop [B] (nullable, build extension): 1 = drop the trajectory from the
+ * update (error / timed-out episodes, whose gradients the paper masks,
+ * PAPER.md:757): its tokens are packed with loss_mask 0 and no action rows,
+ * so it contributes no log-prob work and no gradient and counts as an
+ * all-observation trajectory of its group (loss.py:173-174, :193).
+ * act_off / act_idx then count the remaining action tokens only.
  * Outputs (varlen, packed order, T = n_tokens, A = action tokens):
  *   input_ids[T], loss_mask[T], position_ids[T] (per-trajectory iota),
  *   traj_of_token[T], cu_seqlens[B+1], act_off[B+1], act_idx[A].
  * ---------------------------------------------------------------------- */
 size_t tl_pack_workspace_bytes(int32_t n_traj, int32_t n_seg);
 int tl_pack_varlen(const int32_t* token_pool, const int32_t* seg_src_off, const int32_t* seg_len,
-                   const uint8_t* seg_is_action, const int32_t* traj_seg_off, int32_t n_traj,
-                   int32_t n_seg, int64_t n_tokens, int32_t* input_ids, uint8_t* loss_mask,
+                   const uint8_t* seg_is_action, const int32_t* traj_seg_off,
+                   const uint8_t* traj_drop, int32_t n_traj, int32_t n_seg, int64_t n_tokens, int32_t* input_ids, uint8_t* loss_mask,
                    int32_t* position_ids, int32_t* traj_of_token, int32_t* cu_seqlens,
                    int32_t* act_off, int32_t* act_idx, void* workspace, size_t workspace_bytes,
                    tl_stream_t stream);
@@ -203,12 +210,22 @@ int tl_loss_f32(const float* logp_new, const float* logp_old, const float* logp_
  * backward, on tcgen05/TMEM/TMA.  No reference implementation: contract of
  * PolicyAction.token_logprobs (rollout/policy.py:25-28) / TokenRecord.logp_new
  * (loss.py:30).  hidden row t predicts target input_ids[t] (caller shifts).
- * Only action rows (act_idx) are computed; [T, V] logits are never
- * materialised (vocab is swept in 256-wide tiles with an online
- * log-sum-exp); tokens are processed in chunks of chunk_rows action rows.
+ * Only action rows (act_idx) are computed, in chunks of chunk_rows action
+ * rows.  The forward sweeps the vocabulary in 256-wide tiles with an online
+ * log-sum-exp, so the log-probs never need [T, V] logits.  The backward
+ * needs p = softmax(z) once the final LSE is known: STORE_LOGITS keeps ONE
+ * chunk's logits ([chunk_rows, V] fp16, 46 GB at 4 x 37,888 rows and
+ * V = 152,064) and reuses that buffer for bf16 dS; RECOMPUTE keeps no
+ * logits and recomputes them in a second GEMM.  [T, V] is never allocated.
  * ---------------------------------------------------------------------- */
+/* Workspace of tl_grpo_lmhead_step in the serial modes (STORE_LOGITS,
+ * RECOMPUTE) with the backward: one chunk's [chunk_rows, V] dS buffer, the
+ * split-K tail slices and the step's per-token / per-trajectory state. */
 size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab, int64_t n_tokens,
                                  int32_t n_traj, int32_t n_groups);
+/* Workspace of tl_lmhead_logprobs (forward only: h_c rows + per-row stats,
+ * no dS buffer — ~C*H*2 bytes, 1.1 GB at C = 151,552 rows and H = 3,584). */
+size_t tl_lmhead_logprobs_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab);
 /* Forward only: logp/entropy/lse for rows idx[0..n_rows) of hidden
  * (F3: rollout-side logp_old / logp_ref).  Outputs indexed like idx
  * (out[k] for row idx[k]); idx NULL = rows 0..n_rows-1. */
@@ -245,8 +262,9 @@ size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_
  *   log-prob epilogue; report; loss = -(objective + entropy_coef * mean
  *   entropy); dhidden = dloss/dhidden (bf16 [T, H], observation rows zeroed),
  *   dweight = dloss/dW (fp32 [V, H], overwritten; accumulated with
- *   TL_LMHEAD_ACCUMULATE_DW).  dhidden/dweight NULL =
- *   forward + report only. */
+ *   TL_LMHEAD_ACCUMULATE_DW).  dweight NULL = frozen LM head (dS and dH
+ *   only, 4*T_act*H*V issued FLOPs in store mode); dhidden NULL = detached
+ *   hidden states (dW only); both NULL = forward + report only. */
 int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const int32_t* input_ids,
                         const uint8_t* loss_mask, const int32_t* act_idx, int64_t n_act,
                         const int32_t* traj_of_token, const int32_t* cu_seqlens,

@@ -12,6 +12,9 @@ contract, stated once here and in DESIGN.md:
   act_idx[k]        packed position of the k-th action token (packed order)
   padded [B, Lmax]  row b = trajectory b left-aligned; pad slots get
                     pad_id / mask 0 / position 0
+  drop[b]           (optional) trajectory b keeps its tokens but every mask
+                    bit is 0 — error / timed-out episodes whose gradients the
+                    paper masks; not in the reference code
 """
 
 from __future__ import annotations
@@ -21,12 +24,14 @@ import numpy as np
 from .grpo_oracle import action_mask, flatten
 
 
-def pack_varlen(trajectories):
+def pack_varlen(trajectories, drop=None):
     """trajectories: list of segment lists [(origin, tokens), ...]."""
     ids, mask, pos, tot, cu, act_off, act_idx = [], [], [], [], [0], [0], []
     for b, segs in enumerate(trajectories):
         f = flatten(segs)
         m = action_mask(segs)
+        if drop is not None and drop[b]:
+            m = [0] * len(m)
         base = cu[-1]
         for j, (tok, bit) in enumerate(zip(f, m)):
             ids.append(tok)

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtoolloop_b200.so"
 if os.environ.get("TOOLLOOP_B200_LIB"):
     LIB_PATH = Path(os.environ["TOOLLOOP_B200_LIB"])
 
-TL_ABI_VERSION = 2  # include/toolloop_b200.h
+TL_ABI_VERSION = 3  # include/toolloop_b200.h
 TL_OK = 0
 TL_ERR_INVALID_ARG = 1
 TL_ERR_MASK_MISMATCH = 2
@@ -41,7 +41,8 @@ EXPORTS = [
     "tl_group_advantages", "tl_group_rewards_advantages",
     "tl_loss_f64_workspace_bytes", "tl_loss_f64", "tl_report_f64", "tl_token_ratio_f64",
     "tl_loss_f32_workspace_bytes", "tl_loss_f32",
-    "tl_lmhead_workspace_bytes", "tl_lmhead_step_workspace_bytes", "tl_lmhead_logprobs",
+    "tl_lmhead_workspace_bytes", "tl_lmhead_logprobs_workspace_bytes",
+    "tl_lmhead_step_workspace_bytes", "tl_lmhead_logprobs",
     "tl_grpo_lmhead_step",
     "tl_gemm_bf16",
     "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
@@ -80,7 +81,7 @@ _SIGS = {
     "tl_profile_read": (C.c_int, [_P, _P, _I32]),
     "tl_profile_category": (C.c_char_p, [_I32]),
     "tl_pack_workspace_bytes": (_SZ, [_I32, _I32]),
-    "tl_pack_varlen": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P,
+    "tl_pack_varlen": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _SZ, _P]),
     "tl_pack_padded": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
     "tl_group_advantages": (C.c_int, [_P, _P, _I32, _I32, _D, _P, _I32, _D, _D, _P, _P, _P, _P,
@@ -96,6 +97,7 @@ _SIGS = {
     "tl_loss_f32": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I64,
                               C.POINTER(LossConfigC), _P, _P, _P, _SZ, _P]),
     "tl_lmhead_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I64, _I32, _I32]),
+    "tl_lmhead_logprobs_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
     "tl_lmhead_step_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I64, _I32, _I32, _I32]),
     "tl_lmhead_logprobs": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _I32, _P, _SZ,
                                      _P]),

@@ -362,11 +362,10 @@ struct ChunkWs {
   uint16_t* ds;     // [C, Vld]  fp16 u = (z - m) log2e, then bf16 dS in place
   int16_t* zoff;    // [C, ldo]  int16 slice offsets m of the fp16 u (store mode)
   // step-level
-  float* term;      // [T]
+  float* term;      // [T]  (written at action positions only)
   float* k3o;       // [T]
   uint8_t* flags;   // [T]
-  double* traj_out; // [B*8]
-  double* group_out;// [G*8]
+  ReduceWs red;     // trajectory / group / report reductions
   int* sync;        // [3 * kSyncWaves] wave-lockstep counters (fwd / dH / dW)
   float* tail_part; // [kTailSlots][128][512] split-K tail slices of the dW GEMM
   int* tail_ctr;    // [kTailSlots] slice arrival counters
@@ -444,14 +443,12 @@ ChunkWs carve(Workspace& w, int C, int H, int V, long long T, int B, int G, bool
   c.term = w.take<float>(T);
   c.k3o = w.take<float>(T);
   c.flags = w.take<uint8_t>(T);
-  c.traj_out = w.take<double>(static_cast<size_t>(B) * 8);
-  c.group_out = w.take<double>(static_cast<size_t>(G) * TL_GROUP_OUT_LEN);
+  c.red = carve_reduce(w, T, B, G);
   if (second) {
     second->term = c.term;
     second->k3o = c.k3o;
     second->flags = c.flags;
-    second->traj_out = c.traj_out;
-    second->group_out = c.group_out;
+    second->red = c.red;
   }
   return c;
 }
@@ -544,6 +541,13 @@ extern "C" size_t tl_lmhead_workspace_bytes(int32_t chunk_rows, int32_t hidden, 
                                             int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
   Workspace w{nullptr, 0};
   carve(w, chunk_rows, hidden, vocab, n_tokens, n_traj, n_groups, true);
+  return w.used + 1024;
+}
+
+extern "C" size_t tl_lmhead_logprobs_workspace_bytes(int32_t chunk_rows, int32_t hidden,
+                                                     int32_t vocab) {
+  Workspace w{nullptr, 0};
+  carve(w, chunk_rows, hidden, vocab, 0, 0, 0, false);
   return w.used + 1024;
 }
 
@@ -652,10 +656,10 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(H > 0 && V > 0 && chunk_rows > 0 && n_act >= 0, TL_ERR_INVALID_ARG, "bad sizes");
   TL_REQUIRE(H % 64 == 0, TL_ERR_UNSUPPORTED, "hidden must be a multiple of 64");
-  TL_REQUIRE((dhidden == nullptr) == (dweight == nullptr), TL_ERR_INVALID_ARG,
-             "dhidden and dweight are both given or both NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool bwd = dhidden != nullptr;
+  // backward if either gradient is wanted: dweight NULL = frozen LM head
+  // (dH only), dhidden NULL = detached hidden states (dW only)
+  const bool bwd = dhidden != nullptr || dweight != nullptr;
   Workspace w{static_cast<char*>(workspace), workspace_bytes};
   ChunkWs c2{};
   ChunkWs c = carve(w, chunk_rows, H, V, n_tokens, n_traj, n_groups, bwd,
@@ -668,22 +672,20 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   const double ent_norm = cfg->entropy_norm > 0 ? cfg->entropy_norm : double(n_act);
   const float ent_grad = n_act > 0 ? static_cast<float>(-cfg->entropy_coef / ent_norm) : 0.f;
 
-  // observation rows: zero their term state and (if training) their dH rows
+  // observation rows: logp / entropy 0 and (if training) zero dH rows; their
+  // term / k3 / flags slots are never read (the reductions select by mask)
   if (n_tokens > 0) {
-    cudaMemsetAsync(c.term, 0, n_tokens * sizeof(float), st);
-    cudaMemsetAsync(c.k3o, 0, n_tokens * sizeof(float), st);
-    cudaMemsetAsync(c.flags, 0, n_tokens, st);
     // observation positions report logp 0.0 like cli._flat_logps (cli.py:251)
     cudaMemsetAsync(logp_out, 0, n_tokens * sizeof(float), st);
     cudaMemsetAsync(entropy_out, 0, n_tokens * sizeof(float), st);
-    if (bwd) {
+    if (dhidden) {
       zero_obs_rows_kernel<<<grid_for(n_tokens * H / 8, 256), 256, 0, st>>>(
           loss_mask, n_tokens, H / 8, reinterpret_cast<uint4*>(dhidden));
       TL_LAUNCH_CHECK();
       count_launch();
     }
   }
-  if (bwd && n_act == 0 && !acc_dw) {
+  if (dweight && n_act == 0 && !acc_dw) {
     cudaMemsetAsync(dweight, 0, static_cast<size_t>(V) * H * sizeof(float), st);
   }
 
@@ -757,7 +759,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     const ChunkWs& b = *bufs[i & 1];
     const int rows = rows_of(i);
     const int32_t* ci = act_idx + i * chunk_rows;
-    {
+    if (dhidden) {
       CUtensorMap ma, mb;
       if (int e = make_ab_maps(&ma, &mb, b.ds, false, rows, Vld, weight, true, H, H, V, kCG))
         return e;
@@ -775,6 +777,7 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                                                        PROF_GEMM_DH))
         return e;
     }
+    if (!dweight) return TL_OK;
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
     GemmShape sh = with_sync(
@@ -817,6 +820,5 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     }
   }
   return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,
-                           group_off, n_traj, n_groups, cfg->agg, c.traj_out, c.group_out, report,
-                           st);
+                           group_off, n_traj, n_groups, n_tokens, cfg->agg, c.red, report, st);
 }

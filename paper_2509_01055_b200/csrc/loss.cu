@@ -11,13 +11,12 @@
 //                         tokens bitwise invisible (loss.py:9-10).
 //   report64_kernel       cli.loss aggregation (cli.py:317-345).
 // fp32 performance mode (tl_loss_f32), also the back half of the fused
-// LM-head step:
-//   loss32_traj_kernel    one CTA per trajectory: fp32 terms + scaled
-//                         gradient, fixed-shape tree into per-trajectory sums
-//   traj_reduce_kernel    (LM-head step) per-trajectory tree over per-token
-//                         terms written by the fused log-prob epilogue
-//   group_reduce_kernel   one thread per group (fixed order)
-//   report_kernel         one CTA, fixed order
+// LM-head step — one kernel, loss_unit_kernel (see below):
+//   <compute>  token-parallel 2,048-token units: fp32 terms + scaled gradient
+//   <reduce>   (LM-head step) the same units over the per-token terms written
+//              by the fused log-prob epilogue
+//   and, in the same launch, unit -> trajectory -> group -> report by the
+//   last-arriving CTA of each level.
 // Every reduction has a fixed shape independent of scheduling, so results are
 // run-to-run deterministic; masked tokens are selected, never multiplied.
 #include "exact_fp64.cuh"
@@ -179,256 +178,447 @@ __global__ void ratio64_kernel(const double* __restrict__ a, const double* __res
 
 }  // namespace
 
-// One CTA per trajectory: fixed-shape tree over the trajectory's packed
-// range.  traj_out[b] = {sum term, n_act, clipped, clamps, sum k3, len,
-// sum entropy, 0}.
-__global__ void __launch_bounds__(256)
-    traj_reduce_kernel(const float* __restrict__ term, const float* __restrict__ k3o,
-                       const uint8_t* __restrict__ flags, const float* __restrict__ ent,
-                       const uint8_t* __restrict__ mask, int use_mask,
-                       const int32_t* __restrict__ cu, double* __restrict__ traj_out) {
-  constexpr int kV = 6;
-  __shared__ double sh[kV][256 / 32];
-  const int b = blockIdx.x;
-  const int t0 = cu[b], t1 = cu[b + 1];
-  double v[kV] = {0, 0, 0, 0, 0, 0};  // term, k3, ent, n_act, clipped, clamps
-  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-    if (use_mask && !mask[t]) continue;
-    v[0] += term[t];
-    v[1] += k3o[t];
-    if (ent) v[2] += ent[t];
-    v[3] += 1.0;
-    const uint8_t f = flags[t];
-    v[4] += (f & kFlagClipped) ? 1.0 : 0.0;
-    v[5] += (f & kFlagClamped) ? 1.0 : 0.0;
-  }
+// ---------------------------------------------------------------------------
+// fp32 mode: token-parallel work units + a last-arriver reduction tree.
+//
+// A trajectory of len tokens is cut into max(1, ceil(len / kUnit)) units of
+// kUnit tokens counted from its own start.  Unit c of trajectory b gets the
+// slot  key(b) + c,  key(b) = b + cu[b] / kUnit — injective, with at most
+// n_traj + T / kUnit + 1 slots; the owner of a slot is the last b with
+// key(b) <= slot (key is strictly increasing), so no scan is needed.
+// A persistent grid (a few CTAs per SM) splits the slot range into equal
+// contiguous pieces; a CTA finds the owner of its first slot with one
+// block-wide search, then walks its slots in order, streaming each
+// trajectory's part of the piece (one contiguous token range) through a
+// strided vector loop and reducing it in a fixed-shape tree: the partial
+// goes to the slot of the piece's first unit of that trajectory (the other
+// units' slots get zeros).  The CTA that completes a trajectory (arrival
+// counter per trajectory, counted in units) sums its slots in unit order into
+// traj_out[b]; the one that completes a group sums the group's trajectories
+// (fixed warp tree) into group_out[g]; the one that completes the last group
+// writes the report.  Every sum has a fixed shape (a function of the sizes
+// only), so results are bitwise run-to-run deterministic whichever CTA
+// arrives last; masked-out tokens are selected, never multiplied.
+constexpr int kUnit = 2048;
+constexpr int kUnitThreads = 256;
+constexpr int kUnitCtasPerSm = 4;  // resident CTAs per SM (<= 64 registers)
+constexpr int kRedV = 6;  // term, k3, n_act, clipped, clamps, entropy
+
+__device__ __forceinline__ int unit_key(const int32_t* cu, int b) { return b + cu[b] / kUnit; }
+__device__ __forceinline__ int n_units_of(int len) { return len > kUnit ? (len + kUnit - 1) / kUnit : 1; }
+
+long long unit_slots(long long n_tokens, int n_traj) { return n_traj + n_tokens / kUnit + 1; }
+
+struct UnitArgs {
+  // compute mode (standalone K3): per-token log-probs
+  const float* lnew;
+  const float* lold;
+  const float* lref;
+  const float* adv;
+  const float* traj_w;
+  float* grad;
+  tl_loss_config cfg;
+  // reduce mode (fused LM-head step): per-token terms from the epilogue
+  const float* term;
+  const float* k3o;
+  const uint8_t* flags;
+  const float* ent;
+  // both
+  const uint8_t* mask;
+  int use_mask;
+  int vec_ok;
+  const int32_t* cu;
+  const int32_t* group_off;
+  int n_traj, n_groups, agg;
+  long long n_slots;
+  double* unit_out;   // [slots][8]
+  double* traj_out;   // [n_traj][8]: term, n_act, clipped, clamps, k3, len, entropy, 0
+  double* group_out;  // [n_groups][8]: obj, masked, tokens, clipped, clamps, kl, term, entropy
+  double* report;     // [TL_REPORT_LEN]
+  int* ctr;           // [1] finalize arrival counter (zeroed by the streaming kernel)
+};
+
+template <int N>
+__device__ __forceinline__ void warp_sum(double (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
+
+// Block tree of N doubles per thread -> totals valid in thread 0.  Ends with
+// a barrier, so `sh` can be reused right away.
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double (*sh)[kUnitThreads / 32]) {
+  warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0)
 #pragma unroll
-  for (int i = 0; i < kV; ++i) {
-    double x = v[i];
+    for (int i = 0; i < N; ++i) sh[i][w] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) sh[i][w] = x;
+    for (int i = 0; i < N; ++i) {
+      double x = 0;
+#pragma unroll
+      for (int j = 0; j < kUnitThreads / 32; ++j) x += sh[i][j];
+      v[i] = x;
+    }
+  __syncthreads();
+}
+
+// Last index in [0, n) whose key is <= target (key(0) <= target; key
+// non-decreasing): 256-ary block-wide search.
+template <class Key>
+__device__ __forceinline__ int block_find_key(int n, long long target, Key key) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + blockDim.x - 1) / blockDim.x;
+    const int idx = lo + static_cast<int>(threadIdx.x) * step;
+    const int cnt = __syncthreads_count(idx < hi && key(idx) <= target);
+    lo += (cnt - 1) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// Warp-wide: last g in [0, n) with arr[g] <= x (arr[0] <= x, non-decreasing).
+__device__ __forceinline__ int warp_find_last_le(const int32_t* arr, int n, int x) {
+  int lo = 0, hi = n;
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) / 32;
+    const int idx = lo + lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, idx < hi && arr[idx] <= x);
+    lo += (__popc(m) - 1) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// Finalize (second kernel, launched with programmatic dependent launch so it
+// is resident while the streaming kernel drains): warp w of CTA c owns group
+// g = 8c + w; lane j sums trajectory j's unit slots in unit order into its
+// trajectory row, the warp sums the group's trajectories in a fixed tree into
+// the group row, and the CTA that completes the last group (one arrival
+// counter, zeroed by the streaming kernel) writes the report.
+constexpr int kFinGroupsPerCta = kUnitThreads / 32;
+
+__global__ void __launch_bounds__(kUnitThreads) loss_finalize_kernel(const UnitArgs a) {
+  __shared__ double sh[8][kUnitThreads / 32];
+  __shared__ int sh_flag;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = blockIdx.x * kFinGroupsPerCta + w;
+  if (g < a.n_groups) {
+    const int gb0 = a.group_off[g], gb1 = a.group_off[g + 1];
+    double gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = gb0 + lane; j < gb1; j += 32) {
+      const int t0 = a.cu[j], t1 = a.cu[j + 1];
+      const int s0 = unit_key(a.cu, j), nu = n_units_of(t1 - t0);
+      double tv[kRedV] = {0, 0, 0, 0, 0, 0};
+      for (int u = 0; u < nu; ++u) {
+        const double* uo = a.unit_out + static_cast<long long>(s0 + u) * 8;
+#pragma unroll
+        for (int i = 0; i < kRedV; ++i) tv[i] += uo[i];
+      }
+      double* o = a.traj_out + static_cast<long long>(j) * 8;
+      o[0] = tv[0];
+      o[1] = tv[2];
+      o[2] = tv[3];
+      o[3] = tv[4];
+      o[4] = tv[1];
+      o[5] = t1 - t0;
+      o[6] = tv[5];
+      o[7] = 0;
+      // per-trajectory objective term / n_act, skipped when n = 0 (loss.py:173-174)
+      gv[0] += tv[2] > 0 ? tv[0] / tv[2] : 0.0;
+      gv[1] += tv[2];
+      gv[2] += t1 - t0;
+      gv[3] += tv[3];
+      gv[4] += tv[4];
+      gv[5] += tv[1];
+      gv[6] += tv[0];
+      gv[7] += tv[5];
+    }
+    warp_sum(gv);
+    if (lane == 0) {
+      double* o = a.group_out + static_cast<long long>(g) * 8;
+      o[0] = gv[0] / (gb1 - gb0);
+#pragma unroll
+      for (int i = 1; i < 8; ++i) o[i] = gv[i];
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double r[kV];
-    for (int i = 0; i < kV; ++i) {
-      double x = 0;
-      for (int j = 0; j < (int)(blockDim.x / 32); ++j) x += sh[i][j];
-      r[i] = x;
-    }
-    double* o = traj_out + static_cast<long long>(b) * 8;
-    o[0] = r[0];
-    o[1] = r[3];
-    o[2] = r[4];
-    o[3] = r[5];
-    o[4] = r[1];
-    o[5] = t1 - t0;
-    o[6] = r[2];
-    o[7] = 0;
-  }
-}
-
-// One thread per group; group_out row as in tl_loss_f64.
-__global__ void group_reduce_kernel(const double* __restrict__ traj_out,
-                                    const int32_t* __restrict__ group_off, int n_groups,
-                                    double* __restrict__ group_out) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_groups) return;
-  const int b0 = group_off[g], b1 = group_off[g + 1];
-  double total = 0, masked = 0, tokens = 0, clipped = 0, clamps = 0, kl = 0;
-  for (int b = b0; b < b1; ++b) {
-    const double* t = traj_out + static_cast<long long>(b) * 8;
-    tokens += t[5];
-    if (t[1] == 0) continue;
-    total += t[0] / t[1];
-    masked += t[1];
-    clipped += t[2];
-    clamps += t[3];
-    kl += t[4];
-  }
-  double* o = group_out + static_cast<long long>(g) * TL_GROUP_OUT_LEN;
-  o[0] = total / (b1 - b0);
-  o[1] = masked;
-  o[2] = tokens;
-  o[3] = clipped;
-  o[4] = clamps;
-  o[5] = kl;
-  o[6] = masked > 0 ? clipped / masked : 0.0;
-  o[7] = masked > 0 ? kl / masked : 0.0;
-}
-
-// Batch report (one CTA, fixed-shape tree).  agg = 1 (token-mean):
-// objective = sum(term) / sum(mask).
-__global__ void __launch_bounds__(256)
-    report_kernel(const double* __restrict__ group_out, const double* __restrict__ traj_out,
-                  int n_groups, int n_traj, int agg, double* __restrict__ rep) {
-  constexpr int kV = 8;
-  __shared__ double sh[kV][256 / 32];
-  double v[kV] = {0, 0, 0, 0, 0, 0, 0, 0};  // obj, masked, tokens, clipped, clamps, kl, term, ent
-  for (int g = threadIdx.x; g < n_groups; g += blockDim.x) {
-    const double* o = group_out + static_cast<long long>(g) * TL_GROUP_OUT_LEN;
-    for (int i = 0; i < 6; ++i) v[i] += o[i];
-  }
-  for (int b = threadIdx.x; b < n_traj; b += blockDim.x) {
-    v[6] += traj_out[static_cast<long long>(b) * 8 + 0];
-    v[7] += traj_out[static_cast<long long>(b) * 8 + 6];
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int i = 0; i < kV; ++i) {
-    double x = v[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) sh[i][w] = x;
+    __threadfence();
+    sh_flag = atomicAdd(a.ctr, 1) == static_cast<int>(gridDim.x) - 1;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  double r[kV];
-  for (int i = 0; i < kV; ++i) {
-    double x = 0;
-    for (int j = 0; j < (int)(blockDim.x / 32); ++j) x += sh[i][j];
-    r[i] = x;
+  if (!sh_flag) return;
+  // batch report over all groups (fixed order per thread, then the tree)
+  __threadfence();
+  double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int gg = threadIdx.x; gg < a.n_groups; gg += kUnitThreads) {
+    const double* o = a.group_out + static_cast<long long>(gg) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] += __ldcg(o + i);
   }
+  block_sum(r, sh);
+  if (threadIdx.x != 0) return;
   const double obj = r[0], masked = r[1], term = r[6];
-  rep[0] = agg == 1 ? (masked > 0 ? term / masked : 0.0) : (n_groups ? obj / n_groups : 0.0);
+  double* rep = a.report;
+  rep[0] = a.agg == 1 ? (masked > 0 ? term / masked : 0.0) : (a.n_groups ? obj / a.n_groups : 0.0);
   rep[1] = masked > 0 ? r[3] / masked : 0.0;
   rep[2] = masked;
   rep[3] = masked > 0 ? r[5] / masked : 0.0;
-  rep[4] = n_groups;
-  rep[5] = n_traj;
+  rep[4] = a.n_groups;
+  rep[5] = a.n_traj;
   rep[6] = r[2];
   rep[7] = r[4];
   rep[8] = r[3];
   rep[9] = r[5];
   rep[10] = r[7];
-  rep[11] = agg == 1 ? term : obj;
+  rep[11] = a.agg == 1 ? term : obj;
+  *a.ctr = 0;  // ready for the next launch
 }
 
-// Fused standalone K3 (fp32): one CTA per trajectory computes the per-token
-// terms and gradient and reduces them in a fixed-shape tree straight into
-// traj_out — 13 B/token in (+4 with a reference), 4 B/token out.
-__global__ void __launch_bounds__(256)
-    loss32_traj_kernel(const float* __restrict__ lnew, const float* __restrict__ lold,
-                       const float* __restrict__ lref, const uint8_t* __restrict__ mask,
-                       const int32_t* __restrict__ cu, const float* __restrict__ adv,
-                       const float* __restrict__ traj_w, tl_loss_config cfg,
-                       float* __restrict__ grad, double* __restrict__ traj_out, int vec_ok) {
-  constexpr int kV = 5;
-  __shared__ double sh[kV][256 / 32];
-  const int b = blockIdx.x;
-  const int t0 = cu[b], t1 = cu[b + 1];
-  const float a = adv[b];
-  const float wt = traj_w ? traj_w[b] : 0.f;
-  const float lo = static_cast<float>(1.0 - cfg.eps_low), hi = static_cast<float>(1.0 + cfg.eps_high);
-  const float beta = static_cast<float>(cfg.kl_beta);
-  double v[kV] = {0, 0, 0, 0, 0};  // term, k3, n_act, clipped, clamps
-  auto one = [&](int t, float ln, float lf, float rf, bool act) -> float {
-    if (!act) return 0.f;
-    const TokTermF o = grpo_token_f32(ln, lf, rf, cfg.has_ref != 0 && rf == rf, a, lo, hi, beta,
-                                      cfg.objective);
-    v[0] += o.term;
-    v[1] += o.k3;
-    v[2] += 1.0;
-    v[3] += (o.flags & kFlagClipped) ? 1.0 : 0.0;
-    v[4] += (o.flags & kFlagClamped) ? 1.0 : 0.0;
-    return o.dterm * wt;
-  };
-  auto scalar = [&](int t) {
-    const bool act = !cfg.use_mask || mask[t];
-    const float g = act ? one(t, lnew[t], lold[t], cfg.has_ref ? lref[t] : 0.f, true) : 0.f;
-    if (grad) grad[t] = g;
-  };
-  // 16-byte vectors over the 4-aligned body (observation runs skip their
-  // log-prob loads), scalar head / tail: trajectories start anywhere.
-  const int b0 = (t0 + 3) & ~3, b1 = t1 & ~3;
-  if (!vec_ok || b0 >= b1) {
-    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) scalar(t);
-  } else {
-    if (t0 + static_cast<int>(threadIdx.x) < b0) scalar(t0 + threadIdx.x);
-    if (b1 + static_cast<int>(threadIdx.x) < t1) scalar(b1 + threadIdx.x);
-#pragma unroll 2
-    for (int t = b0 + 4 * threadIdx.x; t < b1; t += 4 * blockDim.x) {
-      const uchar4 m = cfg.use_mask ? *reinterpret_cast<const uchar4*>(mask + t)
-                                    : make_uchar4(1, 1, 1, 1);
-      float4 gr = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m.x | m.y | m.z | m.w) {
-        const float4 ln = *reinterpret_cast<const float4*>(lnew + t);
-        const float4 lf = *reinterpret_cast<const float4*>(lold + t);
-        const float4 rf = cfg.has_ref ? *reinterpret_cast<const float4*>(lref + t)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-        gr.x = one(t, ln.x, lf.x, rf.x, m.x);
-        gr.y = one(t + 1, ln.y, lf.y, rf.y, m.y);
-        gr.z = one(t + 2, ln.z, lf.z, rf.z, m.z);
-        gr.w = one(t + 3, ln.w, lf.w, rf.w, m.w);
+// Streaming kernel: per-token terms (and gradient) over the CTA's contiguous
+// piece of the slot range, one fixed-shape block tree per (piece, trajectory)
+// into the slot of the piece's first unit of that trajectory.
+template <bool kCompute>
+__global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel(const UnitArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int kPark = 16;  // trajectory pieces parked before a block flush
+  constexpr int kWarps = kUnitThreads / 32;
+  __shared__ double park[kPark][kWarps][kRedV];
+  __shared__ int park_slot[kPark], park_units[kPark];
+  int n_park = 0;
+  // sum the parked warp partials in warp order -> the slot of the piece's
+  // first unit of each trajectory, zeros in the slots of the folded units
+  auto flush = [&]() {
+    __syncthreads();
+    for (int j = threadIdx.x; j < n_park; j += kUnitThreads) {
+      double* uo = a.unit_out + static_cast<long long>(park_slot[j]) * 8;
+#pragma unroll
+      for (int i = 0; i < kRedV; ++i) {
+        double x = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) x += park[j][w][i];
+        uo[i] = x;
       }
-      if (grad) *reinterpret_cast<float4*>(grad + t) = gr;
-    }
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      for (int c = 1; c < park_units[j]; ++c)
 #pragma unroll
-  for (int i = 0; i < kV; ++i) {
-    double x = v[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) sh[i][w] = x;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r[kV];
-    for (int i = 0; i < kV; ++i) {
-      double x = 0;
-      for (int j = 0; j < (int)(blockDim.x / 32); ++j) x += sh[i][j];
-      r[i] = x;
+        for (int i = 0; i < kRedV; ++i) uo[c * 8 + i] = 0.0;
     }
-    double* o = traj_out + static_cast<long long>(b) * 8;
-    o[0] = r[0];
-    o[1] = r[2];
-    o[2] = r[3];
-    o[3] = r[4];
-    o[4] = r[1];
-    o[5] = t1 - t0;
-    o[6] = 0;
-    o[7] = 0;
+    __syncthreads();
+    n_park = 0;
+  };
+  const int32_t* cu = a.cu;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.ctr = 0;  // finalize's arrival counter
+  // this CTA's contiguous piece of the slot range
+  const long long s_begin = a.n_slots * blockIdx.x / gridDim.x;
+  const long long s_end = a.n_slots * (blockIdx.x + 1) / gridDim.x;
+  if (s_begin >= s_end) return;
+  int b = block_find_key(a.n_traj, s_begin, [cu](int i) { return unit_key(cu, i); });
+  long long s = s_begin;
+  const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
+  const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
+  const float beta = static_cast<float>(a.cfg.kl_beta);
+  const bool has_ref = kCompute && a.cfg.has_ref != 0;
+  while (s < s_end && b < a.n_traj) {
+    const int t0 = cu[b], t1 = cu[b + 1];
+    const int kb = b + t0 / kUnit, nb = n_units_of(t1 - t0);
+    if (s >= kb + nb) {  // gap slot(s) after trajectory b
+      ++b;
+      continue;
+    }
+    if (s < kb) s = kb;
+    if (s >= s_end) break;
+    const int c0 = static_cast<int>(s - kb);
+    const long long rem = s_end - kb;
+    const int c1 = rem < nb ? static_cast<int>(rem) : nb;
+    const int u0 = min(t1, t0 + c0 * kUnit), u1 = min(t1, t0 + c1 * kUnit);
+
+    // per-thread partials: fp32 sums (a few dozen same-sign terms per thread)
+    // and integer counts; widened to fp64 for the block tree
+    float f_term = 0.f, f_k3 = 0.f, f_ent = 0.f;
+    int n_act = 0, n_clip = 0, n_clamp = 0;
+    float adv = 0.f, wt = 0.f;
+    if constexpr (kCompute) {
+      adv = a.adv[b];
+      wt = a.traj_w ? a.traj_w[b] : 0.f;
+    }
+    auto tok = [&](float x0, float x1, float x2, uint8_t fl, bool act) -> float {
+      if (!act) return 0.f;
+      if constexpr (kCompute) {
+        const TokTermF o = grpo_token_f32(x0, x1, x2, has_ref && x2 == x2, adv, lo, hi, beta,
+                                          a.cfg.objective);
+        f_term += o.term;
+        f_k3 += o.k3;
+        n_act += 1;
+        n_clip += (o.flags & kFlagClipped) ? 1 : 0;
+        n_clamp += (o.flags & kFlagClamped) ? 1 : 0;
+        return o.dterm * wt;
+      } else {
+        f_term += x0;
+        f_k3 += x1;
+        n_act += 1;
+        n_clip += (fl & kFlagClipped) ? 1 : 0;
+        n_clamp += (fl & kFlagClamped) ? 1 : 0;
+        f_ent += x2;
+        return 0.f;
+      }
+    };
+    auto scalar = [&](int t) {
+      const bool act = !a.use_mask || a.mask[t];
+      if constexpr (kCompute) {
+        const float g = act ? tok(a.lnew[t], a.lold[t], has_ref ? a.lref[t] : 0.f, 0, true) : 0.f;
+        if (a.grad) a.grad[t] = g;
+      } else {
+        if (act) tok(a.term[t], a.k3o[t], a.ent ? a.ent[t] : 0.f, a.flags[t], true);
+      }
+    };
+    // 16-byte vectors over the 4-aligned body, scalar head / tail.  The body
+    // runs in batches of kBatch quads per thread: every load of a batch
+    // (masks, then the log-probs of quads with an action token) is issued
+    // before any is consumed, so a thread keeps kBatch x 3 x 16 bytes in
+    // flight instead of one dependent mask -> log-prob round trip per quad.
+    const int b0 = (u0 + 3) & ~3, b1 = u1 & ~3;
+    if (!a.vec_ok || b0 >= b1) {
+      for (int t = u0 + threadIdx.x; t < u1; t += kUnitThreads) scalar(t);
+    } else {
+      if (u0 + static_cast<int>(threadIdx.x) < b0) scalar(u0 + threadIdx.x);
+      if (b1 + static_cast<int>(threadIdx.x) < u1) scalar(b1 + threadIdx.x);
+      constexpr int kBatch = 2;
+      constexpr int kStride = 4 * kUnitThreads;
+      for (int base = b0 + 4 * threadIdx.x; base < b1; base += kBatch * kStride) {
+        uchar4 m[kBatch];
+        float4 x0[kBatch], x1[kBatch], x2[kBatch];
+        uchar4 fl[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          const int t = base + j * kStride;
+          m[j] = t >= b1 ? make_uchar4(0, 0, 0, 0)
+                         : (a.use_mask ? __ldg(reinterpret_cast<const uchar4*>(a.mask + t))
+                                       : make_uchar4(1, 1, 1, 1));
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          const int t = base + j * kStride;
+          const bool any = (m[j].x | m[j].y | m[j].z | m[j].w) != 0;
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (kCompute) {
+            x0[j] = any ? __ldg(reinterpret_cast<const float4*>(a.lnew + t)) : z;
+            x1[j] = any ? __ldg(reinterpret_cast<const float4*>(a.lold + t)) : z;
+            x2[j] = any && has_ref ? __ldg(reinterpret_cast<const float4*>(a.lref + t)) : z;
+            fl[j] = make_uchar4(0, 0, 0, 0);
+          } else {
+            x0[j] = any ? __ldg(reinterpret_cast<const float4*>(a.term + t)) : z;
+            x1[j] = any ? __ldg(reinterpret_cast<const float4*>(a.k3o + t)) : z;
+            x2[j] = any && a.ent ? __ldg(reinterpret_cast<const float4*>(a.ent + t)) : z;
+            fl[j] = any ? __ldg(reinterpret_cast<const uchar4*>(a.flags + t)) : make_uchar4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+          const int t = base + j * kStride;
+          float4 gr;
+          gr.x = tok(x0[j].x, x1[j].x, x2[j].x, fl[j].x, m[j].x);
+          gr.y = tok(x0[j].y, x1[j].y, x2[j].y, fl[j].y, m[j].y);
+          gr.z = tok(x0[j].z, x1[j].z, x2[j].z, fl[j].z, m[j].z);
+          gr.w = tok(x0[j].w, x1[j].w, x2[j].w, fl[j].w, m[j].w);
+          if constexpr (kCompute) {
+            if (t < b1 && a.grad) *reinterpret_cast<float4*>(a.grad + t) = gr;
+          }
+        }
+      }
+    }
+    // warp partial (fixed shuffle tree) parked per (trajectory of the piece,
+    // warp); no block barrier per trajectory — warps run through the piece
+    // independently and the block combines the parked partials in warp order
+    double v[kRedV] = {f_term, f_k3, static_cast<double>(n_act), static_cast<double>(n_clip),
+                       static_cast<double>(n_clamp), f_ent};
+    warp_sum(v);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < kRedV; ++i) park[n_park][threadIdx.x >> 5][i] = v[i];
+    if (threadIdx.x == 0) {
+      park_slot[n_park] = kb + c0;
+      park_units[n_park] = c1 - c0;
+    }
+    if (++n_park == kPark) flush();
+    s = kb + c1;
+    ++b;
   }
+  flush();
 }
 
-int launch_group_report(const double* traj_out, const int32_t* group_off, int n_traj,
-                        int n_groups, int agg, double* group_out, double* report,
-                        cudaStream_t st) {
-  if (n_groups > 0) {
-    group_reduce_kernel<<<(n_groups + 127) / 128, 128, 0, st>>>(traj_out, group_off, n_groups,
-                                                                group_out);
-    TL_LAUNCH_CHECK();
-    count_launch();
+template <bool kCompute>
+int launch_units(UnitArgs a, long long n_tokens, cudaStream_t st) {
+  if (a.n_traj == 0) {  // empty batch: an all-zero report
+    TL_CUDA_TRY(cudaMemsetAsync(a.report, 0, TL_REPORT_LEN * sizeof(double), st));
+    return TL_OK;
   }
-  report_kernel<<<1, 256, 0, st>>>(group_out, traj_out, n_groups, n_traj, agg, report);
+  TL_REQUIRE(a.n_groups > 0, TL_ERR_INVALID_ARG, "trajectories without groups");
+  auto al = [](const void* p, uintptr_t n) { return (reinterpret_cast<uintptr_t>(p) & (n - 1)) == 0; };
+  a.vec_ok = al(a.mask, 4) && al(a.lnew, 16) && al(a.lold, 16) && al(a.lref, 16) && al(a.grad, 16) &&
+             al(a.term, 16) && al(a.k3o, 16) && al(a.flags, 4) && al(a.ent, 16);  // NULL is aligned
+  a.n_slots = unit_slots(n_tokens, a.n_traj);
+#ifndef TL_K3_SLOTS_PER_CTA
+#define TL_K3_SLOTS_PER_CTA 0
+#endif
+  long long ctas = static_cast<long long>(num_sms()) * kUnitCtasPerSm;
+  if (TL_K3_SLOTS_PER_CTA > 0) ctas = (a.n_slots + TL_K3_SLOTS_PER_CTA - 1) / TL_K3_SLOTS_PER_CTA;
+  const unsigned grid = static_cast<unsigned>(a.n_slots < ctas ? a.n_slots : ctas);
+  loss_unit_kernel<kCompute><<<grid, kUnitThreads, 0, st>>>(a);
   TL_LAUNCH_CHECK();
-  count_launch();
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((a.n_groups + kFinGroupsPerCta - 1) / kFinGroupsPerCta);
+  lc.blockDim = dim3(kUnitThreads);
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TL_CUDA_TRY(cudaLaunchKernelEx(&lc, loss_finalize_kernel, a));
+  count_launch(2);
   return TL_OK;
+}
+
+ReduceWs carve_reduce(Workspace& w, long long n_tokens, int n_traj, int n_groups) {
+  ReduceWs r;
+  r.unit_out = w.take<double>(static_cast<size_t>(unit_slots(n_tokens, n_traj)) * 8);
+  r.traj_out = w.take<double>(static_cast<size_t>(n_traj) * 8);
+  r.group_out = w.take<double>(static_cast<size_t>(n_groups) * 8);
+  r.ctr = w.take<int>(1);
+  return r;
 }
 
 int launch_reductions(const float* term, const float* k3o, const uint8_t* flags, const float* ent,
                       const uint8_t* mask, int use_mask, const int32_t* cu, const int32_t* group_off,
-                      int n_traj, int n_groups, int agg, double* traj_out, double* group_out,
+                      int n_traj, int n_groups, long long n_tokens, int agg, const ReduceWs& r,
                       double* report, cudaStream_t st) {
   ProfScope prof(PROF_REDUCE, st);
-  if (n_traj > 0) {
-    traj_reduce_kernel<<<n_traj, 256, 0, st>>>(term, k3o, flags, ent, mask, use_mask, cu, traj_out);
-    TL_LAUNCH_CHECK();
-    count_launch();
-  }
-  if (n_groups > 0) {
-    group_reduce_kernel<<<(n_groups + 127) / 128, 128, 0, st>>>(traj_out, group_off, n_groups,
-                                                                group_out);
-    TL_LAUNCH_CHECK();
-    count_launch();
-  }
-  report_kernel<<<1, 256, 0, st>>>(group_out, traj_out, n_groups, n_traj, agg, report);
-  TL_LAUNCH_CHECK();
-  count_launch();
-  return TL_OK;
+  UnitArgs a{};
+  a.term = term;
+  a.k3o = k3o;
+  a.flags = flags;
+  a.ent = ent;
+  a.mask = mask;
+  a.use_mask = use_mask;
+  a.cu = cu;
+  a.group_off = group_off;
+  a.n_traj = n_traj;
+  a.n_groups = n_groups;
+  a.agg = agg;
+  a.unit_out = r.unit_out;
+  a.traj_out = r.traj_out;
+  a.group_out = r.group_out;
+  a.report = report;
+  a.ctr = r.ctr;
+  return launch_units<false>(a, n_tokens, st);
 }
 
 }  // namespace tl
@@ -506,10 +696,8 @@ extern "C" int tl_token_ratio_f64(const double* logp_new, const double* logp_old
 }
 
 extern "C" size_t tl_loss_f32_workspace_bytes(int64_t n_tokens, int32_t n_traj, int32_t n_groups) {
-  (void)n_tokens;
   tl::Workspace w{nullptr, 0};
-  w.take<double>(static_cast<size_t>(n_traj) * 8);
-  w.take<double>(static_cast<size_t>(n_groups) * TL_GROUP_OUT_LEN);
+  tl::carve_reduce(w, n_tokens, n_traj, n_groups);
   return w.used + 256;
 }
 
@@ -524,22 +712,31 @@ extern "C" int tl_loss_f32(const float* logp_new, const float* logp_old, const f
   TL_REQUIRE(!cfg->has_ref || logp_ref, TL_ERR_INVALID_ARG, "has_ref without logp_ref");
   TL_REQUIRE(!cfg->use_mask || mask, TL_ERR_INVALID_ARG, "use_mask without mask");
   TL_REQUIRE(!grad || traj_w, TL_ERR_INVALID_ARG, "grad requires traj_w");
-  (void)traj_of_token;  // the fused kernel walks trajectories via cu_seqlens
+  (void)traj_of_token;  // units walk trajectories via cu_seqlens
   tl::Workspace w{static_cast<char*>(workspace), workspace_bytes};
-  double* traj_out = w.take<double>(static_cast<size_t>(n_traj) * 8);
-  double* group_out = w.take<double>(static_cast<size_t>(n_groups) * TL_GROUP_OUT_LEN);
+  const tl::ReduceWs r = tl::carve_reduce(w, n_tokens, n_traj, n_groups);
   TL_REQUIRE(w.ok(), TL_ERR_WORKSPACE, "loss_f32 workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   tl::ProfScope prof(tl::PROF_LOSS, st);
-  if (n_traj > 0) {
-    auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
-    const int vec_ok = al(logp_new, 16) && al(logp_old, 16) && al(logp_ref, 16) &&
-                       al(grad, 16) && al(mask, 4);  // NULL pointers are aligned
-    tl::loss32_traj_kernel<<<n_traj, 256, 0, st>>>(logp_new, logp_old, logp_ref, mask, cu_seqlens,
-                                                   adv32, traj_w, *cfg, grad, traj_out, vec_ok);
-    TL_LAUNCH_CHECK();
-    tl::count_launch();
-  }
-  return tl::launch_group_report(traj_out, group_off, n_traj, n_groups, cfg->agg, group_out, report,
-                                 st);
+  tl::UnitArgs a{};
+  a.lnew = logp_new;
+  a.lold = logp_old;
+  a.lref = cfg->has_ref ? logp_ref : nullptr;
+  a.adv = adv32;
+  a.traj_w = traj_w;
+  a.grad = grad;
+  a.cfg = *cfg;
+  a.mask = mask;
+  a.use_mask = cfg->use_mask;
+  a.cu = cu_seqlens;
+  a.group_off = group_off;
+  a.n_traj = n_traj;
+  a.n_groups = n_groups;
+  a.agg = cfg->agg;
+  a.unit_out = r.unit_out;
+  a.traj_out = r.traj_out;
+  a.group_out = r.group_out;
+  a.report = report;
+  a.ctr = r.ctr;
+  return tl::launch_units<true>(a, n_tokens, st);
 }

@@ -62,6 +62,66 @@ def _group_sizes(group_off) -> np.ndarray:
     return np.diff(go)
 
 
+def _check_groups(go: np.ndarray, n_rewards: int | None, n_traj: int | None) -> None:
+    """Host-side shape checks before any launch (the reference raises
+    MaskMismatch for these length mismatches, loss.py:45-49, :85-90)."""
+    from .errors import MaskMismatch
+
+    if go.ndim != 1 or len(go) < 1 or go[0] != 0 or np.any(np.diff(go) < 0):
+        raise ValueError("group_off must be a non-decreasing offset array starting at 0")
+    if n_rewards is not None and n_rewards != int(go[-1]):
+        raise MaskMismatch(f"{n_rewards} rewards for {int(go[-1])} trajectories in group_off")
+    if n_traj is not None and n_traj != int(go[-1]):
+        raise MaskMismatch(f"group_off covers {int(go[-1])} trajectories, the batch has {n_traj}")
+
+
+def _check_tensor(name: str, t, dtype, n: int | None, device, *, rank: int = 1) -> None:
+    """Every tensor handed to the C ABI: dtype, contiguity, device and length
+    (a float64 log-prob tensor would otherwise be reinterpreted as float32)."""
+    if t is None:
+        return
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if t.dim() != rank:
+        raise ValueError(f"{name} must have {rank} dimension(s), got shape {tuple(t.shape)}")
+    if n is not None and t.shape[0] != n:
+        from .errors import MaskMismatch
+
+        raise MaskMismatch(f"{name} has {t.shape[0]} entries, expected {n}")
+
+
+def _on(stream):
+    """Run the host side of an operator with `stream` as torch's current
+    stream, so its temporaries are allocated (and freed) in that stream's
+    order and the final report read (.cpu()) is ordered after the kernels."""
+    import contextlib
+
+    import torch
+
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+def _stream_scoped(fn):
+    """Operators taking `stream=`: the whole host side runs under _on(stream)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        with _on(kwargs.get("stream")):
+            return fn(*args, **kwargs)
+
+    return wrapped
+
+
+def _n_rewards(rewards) -> int:
+    return int(rewards.numel()) if hasattr(rewards, "numel") else len(rewards)
+
+
+@_stream_scoped
 def advantages(rewards, group_off, n_act_per_traj=None, *, std_floor: float = 1e-6,
                agg: int = 0, norm_groups: float | None = None, norm_tokens: float | None = None,
                act_off=None, device=None, stream=None):
@@ -71,6 +131,7 @@ def advantages(rewards, group_off, n_act_per_traj=None, *, std_floor: float = 1e
 
     L = _lib.lib()
     go = np.asarray(group_off, dtype=np.int32)
+    _check_groups(go, _n_rewards(rewards), None)
     sizes = _group_sizes(go)
     if np.any(sizes < 2):
         from .errors import GroupTooSmall
@@ -169,17 +230,25 @@ class GRPOStep:
                  logp_ref=None, *, backward: bool = True, norm_groups: float | None = None,
                  norm_tokens: float | None = None, stream=None, outputs=None,
                  adv_cache=None, sync_report: bool = True,
-                 accumulate_dweight: bool = False) -> StepResult:
+                 accumulate_dweight: bool = False, want_dhidden: bool = True,
+                 want_dweight: bool = True) -> StepResult:
         """One step over `packed`.  Micro-batching an optimizer step: call once
         per micro-batch with the step's global norm_groups / norm_tokens and
         accumulate_dweight=True after the first (outputs["dweight"] reused),
-        then combine the reports with parallel.combine_reports."""
-        plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
-                             backward=backward, norm_groups=norm_groups, norm_tokens=norm_tokens,
-                             outputs=outputs, adv_cache=adv_cache,
-                             accumulate_dweight=accumulate_dweight)
-        self._launch(plan, stream)
-        return plan.result(sync_report)
+        then combine the reports with parallel.combine_reports.
+        want_dweight=False: frozen LM head (dS + dH only, no dW GEMM);
+        want_dhidden=False: dW only.  `stream`: a torch.cuda.Stream to run on
+        (temporaries are allocated in its order; the report read waits on it)."""
+        with _on(stream):
+            plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
+                                 backward=backward, norm_groups=norm_groups,
+                                 norm_tokens=norm_tokens, outputs=outputs, adv_cache=adv_cache,
+                                 accumulate_dweight=accumulate_dweight,
+                                 want_dhidden=want_dhidden, want_dweight=want_dweight)
+            if stream is not None:
+                plan.ws.record_stream(stream)
+            self._launch(plan, stream)
+            return plan.result(sync_report)
 
     def capture(self, packed: PackedBatch, group_off, rewards, hidden, weight, logp_old,
                 logp_ref=None, *, norm_groups: float | None = None,
@@ -192,7 +261,8 @@ class GRPOStep:
 
         plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
                              backward=True, norm_groups=norm_groups, norm_tokens=norm_tokens,
-                             outputs=outputs, adv_cache=None, accumulate_dweight=False)
+                             outputs=outputs, adv_cache=None, accumulate_dweight=False,
+                             want_dhidden=True, want_dweight=True)
         if plan.rewards.data_ptr() != getattr(rewards, "data_ptr", lambda: -1)():
             raise ValueError("capture() needs rewards as a float64 device tensor (static input)")
         side = torch.cuda.Stream(device=hidden.device)
@@ -206,7 +276,8 @@ class GRPOStep:
         return CapturedStep(graph, plan)
 
     def _prepare(self, packed, group_off, rewards, hidden, weight, logp_old, logp_ref, *,
-                 backward, norm_groups, norm_tokens, outputs, adv_cache, accumulate_dweight):
+                 backward, norm_groups, norm_tokens, outputs, adv_cache, accumulate_dweight,
+                 want_dhidden, want_dweight):
         import torch
 
         L = _lib.lib()
@@ -216,14 +287,17 @@ class GRPOStep:
         if hidden.shape != (packed.n_tokens, self.H) or weight.shape != (self.V, self.H):
             raise ValueError(f"hidden {tuple(hidden.shape)} / weight {tuple(weight.shape)} do not "
                              f"match T={packed.n_tokens}, H={self.H}, V={self.V}")
-        if logp_old.shape[0] != packed.n_tokens or (logp_ref is not None and
-                                                    logp_ref.shape[0] != packed.n_tokens):
-            from .errors import MaskMismatch
-
-            raise MaskMismatch("logp arrays must have one entry per packed token")
+        _check_tensor("hidden", hidden, torch.bfloat16, packed.n_tokens, dev, rank=2)
+        _check_tensor("weight", weight, torch.bfloat16, self.V, dev, rank=2)
+        _check_tensor("logp_old", logp_old, torch.float32, packed.n_tokens, dev)
+        _check_tensor("logp_ref", logp_ref, torch.float32, packed.n_tokens, dev)
+        for k in ("input_ids", "loss_mask", "act_idx", "traj_of_token", "cu_seqlens", "act_off"):
+            if getattr(packed, k).device != dev:
+                raise ValueError(f"packed.{k} is on {getattr(packed, k).device}, expected {dev}")
         cfg = self.cfg
         agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
         go = np.asarray(group_off, dtype=np.int32)
+        _check_groups(go, _n_rewards(rewards) if adv_cache is None else None, packed.n_traj)
         n_groups = len(go) - 1
         plan = _StepPlan()
         plan.L = L
@@ -262,8 +336,10 @@ class GRPOStep:
         plan.T = T
         plan.logp = buf("logp", max(T, 1), torch.float32)
         plan.ent = buf("entropy", max(T, 1), torch.float32)
-        plan.dh = buf("dhidden", (T, self.H), torch.bfloat16) if backward else None
-        plan.dw = buf("dweight", (self.V, self.H), torch.float32) if backward else None
+        plan.dh = buf("dhidden", (T, self.H), torch.bfloat16) if backward and want_dhidden else None
+        plan.dw = buf("dweight", (self.V, self.H), torch.float32) if backward and want_dweight else None
+        _check_tensor("outputs['dhidden']", plan.dh, torch.bfloat16, T, dev, rank=2)
+        _check_tensor("outputs['dweight']", plan.dw, torch.float32, self.V, dev, rank=2)
         plan.rep = buf("report", _lib.TL_REPORT_LEN, torch.float64)
         chunk = self._chunk(packed.n_act, T, packed.n_traj, n_groups, dev)
         self.last_chunk = chunk
@@ -323,6 +399,7 @@ class CapturedStep:
         return self.plan.result(sync_report)
 
 
+@_stream_scoped
 def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_ref=None,
               cfg: LossConfig | None = None, *, want_grad: bool = True, stream=None):
     """Standalone fp32 K3 over a packed batch with given logp_new (e.g. from a
@@ -332,8 +409,11 @@ def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_
     L = _lib.lib()
     cfg = cfg or LossConfig()
     dev = logp_new.device
+    for k, t in (("logp_new", logp_new), ("logp_old", logp_old), ("logp_ref", logp_ref)):
+        _check_tensor(k, t, torch.float32, packed.n_tokens, dev)
     agg = 1 if cfg.loss_agg == AGG_TOKEN_MEAN else 0
     go = np.asarray(group_off, dtype=np.int32)
+    _check_groups(go, _n_rewards(rewards), packed.n_traj)
     n_groups = len(go) - 1
     _, adv32, traj_w, _, d_go = advantages(rewards, go, std_floor=cfg.std_floor, agg=agg,
                                            norm_tokens=max(packed.n_act, 1),
@@ -352,6 +432,7 @@ def grpo_loss(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_
     return report_dict(rep.cpu()), (grad[:T] if want_grad else None)
 
 
+@_stream_scoped
 def report_f64(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp_ref=None,
                cfg: LossConfig | None = None, stream=None) -> dict:
     """cli.loss's report (cli.py:309-345) for a whole packed batch in the fp64
@@ -363,7 +444,10 @@ def report_f64(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp
     L = _lib.lib()
     cfg = cfg or LossConfig()
     dev = packed.cu_seqlens.device
+    for k, t in (("logp_new", logp_new), ("logp_old", logp_old), ("logp_ref", logp_ref)):
+        _check_tensor(k, t, torch.float64, packed.n_tokens, dev)
     go = np.asarray(group_off, dtype=np.int32)
+    _check_groups(go, _n_rewards(rewards), packed.n_traj)
     n_groups = len(go) - 1
     adv64, _, _, _, d_go = advantages(rewards, go, std_floor=cfg.std_floor, device=dev,
                                       stream=stream)
@@ -382,6 +466,7 @@ def report_f64(packed: PackedBatch, group_off, rewards, logp_new, logp_old, logp
     return report_dict(rep.cpu())
 
 
+@_stream_scoped
 def lmhead_logprobs(hidden, weight, targets, rows=None, *, chunk_rows: int | None = None,
                     stream=None):
     """Forward-only fused LM head (F3: rollout-side logp_old / logp_ref).
@@ -393,9 +478,20 @@ def lmhead_logprobs(hidden, weight, targets, rows=None, *, chunk_rows: int | Non
     V = weight.shape[0]
     n = hidden.shape[0] if rows is None else rows.shape[0]
     dev = hidden.device
-    # forward-only workspace is small (h_c + per-row stats): always the largest chunk
+    _check_tensor("hidden", hidden, torch.bfloat16, None, dev, rank=2)
+    _check_tensor("weight", weight, torch.bfloat16, None, dev, rank=2)
+    if weight.shape[1] != H:
+        raise ValueError(f"weight {tuple(weight.shape)} does not match hidden dim {H}")
+    _check_tensor("targets", targets, torch.int32, None, dev)
+    _check_tensor("rows", rows, torch.int32, None, dev)
+    if rows is None and targets.shape[0] < n:
+        from .errors import MaskMismatch
+
+        raise MaskMismatch(f"{targets.shape[0]} targets for {n} hidden rows")
+    # forward-only workspace is small (h_c + per-row stats, no dS buffer):
+    # always the largest chunk
     chunk = int(chunk_rows or min(MAX_CHUNK_MULT * DEFAULT_CHUNK_ROWS, max(128, (n + 127) // 128 * 128)))
-    ws_bytes = int(L.tl_lmhead_workspace_bytes(chunk, H, V, 0, 0, 0))
+    ws_bytes = int(L.tl_lmhead_logprobs_workspace_bytes(chunk, H, V))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     logp = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
     ent = torch.empty(max(n, 1), dtype=torch.float32, device=dev)

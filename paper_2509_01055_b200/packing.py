@@ -45,6 +45,13 @@ class SegmentTable:
     def n_act(self) -> int:
         return int(self.seg_len[self.seg_is_action.astype(bool)].sum(dtype=np.int64))
 
+    def n_act_kept(self, drop=None) -> int:
+        """Action tokens left after dropping trajectories (drop: [B] bool)."""
+        if drop is None:
+            return self.n_act
+        keep = ~np.repeat(np.asarray(drop, dtype=bool), np.diff(self.traj_seg_off))
+        return int(self.seg_len[self.seg_is_action.astype(bool) & keep].sum(dtype=np.int64))
+
     def traj_lengths(self) -> np.ndarray:
         c = np.concatenate([[0], np.cumsum(self.seg_len, dtype=np.int64)])
         return c[self.traj_seg_off[1:]] - c[self.traj_seg_off[:-1]]
@@ -118,16 +125,27 @@ def _dev(a: np.ndarray, device, non_blocking: bool = False):
 
 
 def pack_table(table: SegmentTable, device=None, stream=None, validate: bool = True,
-               vocab: int | None = None, device_inputs: dict | None = None) -> PackedBatch:
+               vocab: int | None = None, device_inputs: dict | None = None,
+               drop=None) -> PackedBatch:
     """Pack a segment table on the GPU.  `device_inputs` may supply the table
-    columns already resident on the device (keys as SegmentTable fields)."""
+    columns already resident on the device (keys as SegmentTable fields).
+    drop ([B] bool, optional): trajectories dropped from the update (error /
+    timed-out episodes) — packed with loss_mask 0 and no action
+    rows, so they add no LM-head work and no gradient but still count in their
+    group (as an all-observation trajectory, loss.py:173-174)."""
     import torch
 
     L = _lib.lib()
     if validate:
         table.validate(vocab)
+        if drop is not None and len(drop) != table.n_traj:
+            raise ValueError(f"drop has {len(drop)} entries for {table.n_traj} trajectories")
     device = torch.device(device or "cuda")
-    B, S, T, A = table.n_traj, table.n_seg, table.n_tokens, table.n_act
+    B, S, T = table.n_traj, table.n_seg, table.n_tokens
+    A = table.n_act_kept(drop)
+    d_drop = None
+    if drop is not None:
+        d_drop = _dev(np.asarray(drop, dtype=np.uint8), device)
     d = device_inputs or {}
     pool = d.get("token_pool")
     if pool is None:
@@ -154,16 +172,17 @@ def pack_table(table: SegmentTable, device=None, stream=None, validate: bool = T
     ws_bytes = L.tl_pack_workspace_bytes(B, S)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     _lib.check(L.tl_pack_varlen(
-        pool.data_ptr(), src.data_ptr(), ln.data_ptr(), isa.data_ptr(), tso.data_ptr(), B, S, T,
+        pool.data_ptr(), src.data_ptr(), ln.data_ptr(), isa.data_ptr(), tso.data_ptr(),
+        _lib.ptr(d_drop), B, S, T,
         out.input_ids.data_ptr(), out.loss_mask.data_ptr(), out.position_ids.data_ptr(),
         out.traj_of_token.data_ptr(), out.cu_seqlens.data_ptr(), out.act_off.data_ptr(),
         out.act_idx.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_handle(stream)))
     return out
 
 
-def pack(trajectories: Sequence[Trajectory], device=None, stream=None) -> PackedBatch:
+def pack(trajectories: Sequence[Trajectory], device=None, stream=None, drop=None) -> PackedBatch:
     """Pack Trajectory objects (varlen, packed order) on the GPU."""
-    return pack_table(segment_table(trajectories), device=device, stream=stream)
+    return pack_table(segment_table(trajectories), device=device, stream=stream, drop=drop)
 
 
 def pad(packed: PackedBatch, lmax: int | None = None, pad_id: int = 0, stream=None):

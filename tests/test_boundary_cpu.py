@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"missing export {s}"
     assert set(syms) == set(_lib.EXPORTS)
-    assert lib.tl_abi_version() == _lib.TL_ABI_VERSION == 2
+    assert lib.tl_abi_version() == _lib.TL_ABI_VERSION == 3
     assert lib.tl_launch_count() >= 0
 
 
@@ -40,6 +40,9 @@ def test_workspace_queries_are_host_only():
     assert lib.tl_loss_f64_workspace_bytes(1000) >= 1000 * 25
     big = lib.tl_lmhead_workspace_bytes(37888, 3584, 152064, 6_000_000, 2048, 256)
     assert big > 37888 * 152064 * 2  # holds the bf16 dS chunk
+    # forward-only (F3) workspace: no dS chunk, ~ the gathered rows only
+    fwd = lib.tl_lmhead_logprobs_workspace_bytes(4 * 37888, 3584, 152064)
+    assert 4 * 37888 * 3584 * 2 <= fwd < 4 * 37888 * 3584 * 2 * 1.1
 
 
 def test_config_validation_matches_reference():

@@ -41,12 +41,15 @@ def timed(fn, iters=None):
 
 def device_ms(fn, cat, iters=5):
     """Median device time of the kernels `fn` launches in profile category
-    `cat` (CUDA events recorded by the library around its own launches, so
-    host / Python / allocation time is excluded); L2 flushed before each."""
+    `cat` (CUDA events recorded by the library around its own launches);
+    L2 flushed before each.  A ~1 ms spin kernel runs first so the host has
+    queued every launch before the GPU reaches them: the kernels run back to
+    back and the events measure device time, not host submission latency."""
     ts = []
     for _ in range(iters):
         FLUSH.fill_(1)
         torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
         _lib.profile_enable(True)
         fn()
         torch.cuda.synchronize()
