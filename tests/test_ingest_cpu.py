@@ -12,6 +12,7 @@ from paper_2509_01055_b200 import cli
 from paper_2509_01055_b200.errors import EpisodeLogError, MaskMismatch
 from paper_2509_01055_b200.ingest import ingest
 from paper_2509_01055_b200.packing import segment_table
+from oracle import episodes_oracle as EO  # noqa: E402  (checker)
 
 
 def _files(tmp_path, golden_cli):
@@ -23,17 +24,17 @@ def _files(tmp_path, golden_cli):
 
 
 def _python_path(ep, sc=None):
-    recs = cli.read_episodes(ep)
+    recs = EO.read_episodes(ep)
     order = {}
     for i, r in enumerate(recs):
         order.setdefault(r["task_id"], []).append(i)
     perm = [i for v in order.values() for i in v]
     tab = segment_table([recs[i]["trajectory"] for i in perm])
     if sc is None:
-        new = [cli.flat_logps(recs[i]) for i in perm]
+        new = [EO.flat_logps(recs[i]) for i in perm]
         old, ref = new, None
     else:
-        side = cli.read_sidecar(sc, len(recs))
+        side = EO.read_sidecar(sc, len(recs))
         new = [side[i]["logp_new"] for i in perm]
         old = [side[i].get("logp_old", side[i]["logp_new"]) for i in perm]
         ref = [side[i].get("logp_ref") for i in perm]
