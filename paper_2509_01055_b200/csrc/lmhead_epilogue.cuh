@@ -187,18 +187,24 @@ struct EpiLseStats {
     __half_raw* dst = keep ? p.zout + static_cast<long long>(row) * p.ldz + cb : nullptr;
     float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
     if (nvalid >= 32) {
+      // even / odd columns as the two lanes of packed fp32 pairs (FFMA2 /
+      // FADD2: same bits as the scalar split accumulators, half the issues)
       uint32_t hq[16];
+      const float2 l2 = make_float2(kLog2e, kLog2e), nmb = make_float2(-mb, -mb);
+      float2 s2 = make_float2(0.f, 0.f), t2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        const float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
-        const float u0 = fmaf(v0, kLog2e, -mb), u1 = fmaf(v1, kLog2e, -mb);
-        const float e0 = ex2_ftz(u0), e1 = ex2_ftz(u1);
-        s0 += e0;
-        s1 += e1;
-        t0 = fmaf(e0, v0, t0);
-        t1 = fmaf(e1, v1, t1);
-        hq[j / 2] = pack_f16x2_sat(u0, u1);
+        const float2 v = make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+        const float2 u = ffma2(v, l2, nmb);
+        const float2 e = make_float2(ex2_ftz(u.x), ex2_ftz(u.y));
+        s2 = fadd2(s2, e);
+        t2 = ffma2(e, v, t2);
+        hq[j / 2] = pack_f16x2_sat(u.x, u.y);
       }
+      s0 = s2.x;
+      s1 = s2.y;
+      t0 = t2.x;
+      t1 = t2.y;
       if (keep) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)

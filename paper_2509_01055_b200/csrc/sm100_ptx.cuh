@@ -110,6 +110,31 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
+// Packed fp32 pairs (sm_100+: FFMA2 / FADD2 / FMUL2 — one instruction for two
+// lanes of IEEE round-to-nearest fp32 math, so results are bitwise those of
+// the scalar fmaf / + / *; half the issue slots in the epilogues).
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) {
+  return *reinterpret_cast<unsigned long long*>(&a);
+}
+__device__ __forceinline__ float2 bits_f2(unsigned long long a) {
+  return *reinterpret_cast<float2*>(&a);
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+
 // ------------------------------------------------ epilogue global stores ----
 // Fire-and-forget fp32 vector add into global memory, performed at L2
 // (red.global.add.v4.f32, sm_90+): an accumulate epilogue never waits on a

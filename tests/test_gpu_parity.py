@@ -9,7 +9,7 @@ Tolerances:
   fp32 loss/adv     rel 1e-5 (north star)
   LM-head logp      abs 1e-4 vs an fp64 oracle on identical bf16 inputs
                     (small shapes and sampled rows at the full C2 shape)
-  dH / dW           rel Frobenius 2e-2 (dS rounded to bf16)
+  dH / dW           rel Frobenius 5e-3 (dS rounded to bf16; measured ~2e-3)
 """
 
 import math
@@ -361,6 +361,25 @@ def _rel_fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
+# dH / dW against the fp64 oracle: dS is rounded to bf16 (2^-9 relative) before
+# the dH / dW GEMMs, so the relative Frobenius error sits near 2e-3 (measured
+# 1.4e-3 .. 2.4e-3 at the full C2 / C5 shapes, profiles/r2a_bwd_fullshape_parity.jsonl).
+BWD_TOL = 5e-3
+
+
+def _bwd_err(name, got, ref):
+    """Relative Frobenius error, recorded to gpurun_out/bwd_small_parity.jsonl."""
+    import json
+    import os
+
+    e = _rel_fro(got, ref)
+    out = os.path.join(os.path.dirname(__file__), "..", "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "bwd_small_parity.jsonl"), "a") as fh:
+            fh.write(json.dumps({"test": name, "rel_fro": e, "tol": BWD_TOL}) + "\n")
+    return e
+
+
 MODES = {"store": {}, "recompute": {"recompute": True}, "pipelined": {"pipelined": True}}
 
 
@@ -413,9 +432,9 @@ def test_grpo_lmhead_step_vs_oracle(H, V, chunk, mode):
     cg = np.full(len(act), -0.01 / len(act))
     dH, dW = LH.lmhead_backward(hn[act], Wn, ids[act], gl[act], cg)
     got_dh = res.dhidden.float().cpu().numpy()
-    assert _rel_fro(got_dh[act], dH) <= 2e-2
+    assert _bwd_err(f"step_{mode}_H{H}_V{V}_c{chunk}_dH", got_dh[act], dH) <= BWD_TOL
     assert np.all(got_dh[packed.loss_mask.cpu().numpy() == 0] == 0)
-    assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
+    assert _bwd_err(f"step_{mode}_H{H}_V{V}_c{chunk}_dW", res.dweight.cpu().numpy(), dW) <= BWD_TOL
 
 
 def test_grpo_lmhead_step_dapo_token_mean():
@@ -456,8 +475,8 @@ def test_grpo_lmhead_step_dapo_token_mean():
     obj = sum(terms) / len(act)
     assert abs(res.report["objective"] - obj) <= 1e-4
     dH, dW = LH.lmhead_backward(hn[act], Wn, ids[act], -grads[act] / len(act))
-    assert _rel_fro(res.dhidden.float().cpu().numpy()[act], dH) <= 2e-2
-    assert _rel_fro(res.dweight.cpu().numpy(), dW) <= 2e-2
+    assert _bwd_err("dapo_dH", res.dhidden.float().cpu().numpy()[act], dH) <= BWD_TOL
+    assert _bwd_err("dapo_dW", res.dweight.cpu().numpy(), dW) <= BWD_TOL
 
 
 @pytest.mark.parametrize("agg", ["seq-mean-token-mean", "token-mean"])
@@ -677,4 +696,4 @@ def test_dw_split_k_tail_vs_oracle():
                 pos += 1
     cg = np.full(len(act), -0.01 / len(act))
     _, dW = LH.lmhead_backward(hn[act], Wn, ids[act], gl[act], cg)
-    assert _rel_fro(dw1.cpu().numpy(), dW) <= 2e-2
+    assert _bwd_err("dw_split_tail_dW", dw1.cpu().numpy(), dW) <= BWD_TOL
