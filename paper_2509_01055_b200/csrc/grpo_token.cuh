@@ -57,4 +57,46 @@ __device__ __forceinline__ TokTermF grpo_token_f32(float lnew, float lold, float
   return o;
 }
 
+// The same arithmetic with the reference / objective choices as template
+// parameters and the diagnostics as booleans (the standalone K3 streaming
+// kernel: no per-token branches on the config, no flag-byte round trip).
+// A NaN reference log-prob (TokenRecord.logp_ref is None) is selected out.
+struct TokTermB {
+  float term, k3, dterm;
+  bool clipped, clamped;
+};
+
+template <bool kRef, int kObjective>
+__device__ __forceinline__ TokTermB grpo_token_t(float lnew, float lold, float lref, float adv,
+                                                 float lo, float hi, float beta) {
+  TokTermB o;
+  const float d = lnew - lold;
+  o.clamped = d > kClampF || d < -kClampF;
+  const float dc = fminf(fmaxf(d, -kClampF), kClampF);
+  const float r = expf(dc);
+  const float ra = r * adv;
+  if constexpr (kObjective == 0) {
+    const float ca = fminf(fmaxf(r, lo), hi) * adv;
+    o.term = ca < ra ? ca : ra;
+    o.clipped = (r > hi && adv > 0.f) || (r < lo && adv < 0.f);
+    o.dterm = (!o.clamped && ra <= ca) ? ra : 0.f;
+  } else {
+    o.term = ra;
+    o.clipped = false;
+    o.dterm = o.clamped ? 0.f : ra;
+  }
+  o.k3 = 0.f;
+  if constexpr (kRef) {
+    const bool ok = lref == lref;
+    const float e = lref - lnew;
+    const float ec = fminf(fmaxf(e, -kClampF), kClampF);
+    const float ee = expf(ec);
+    const float k3 = (ee - ec) - 1.f;
+    o.k3 = ok ? k3 : 0.f;
+    o.term = ok ? o.term - beta * k3 : o.term;
+    o.dterm = (ok && e >= -kClampF && e <= kClampF) ? o.dterm + beta * (ee - 1.f) : o.dterm;
+  }
+  return o;
+}
+
 }  // namespace tl

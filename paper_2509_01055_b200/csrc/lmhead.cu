@@ -233,6 +233,7 @@ __device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float K, float A, 
                                            float gg) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
   float d[8];
+#if TL_EPI_F32X2
   const float2 K2 = make_float2(K, K), A2 = make_float2(A, A), B2 = make_float2(B, B);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {  // packed fp32 pairs: bitwise the scalar math
@@ -242,6 +243,14 @@ __device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float K, float A, 
     d[2 * k] = pd.x;
     d[2 * k + 1] = pd.y;
   }
+#else
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 u = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+    d[2 * k] = ex2_ftz(u.x + K) * fmaf(B, u.x, A);
+    d[2 * k + 1] = ex2_ftz(u.y + K) * fmaf(B, u.y, A);
+  }
+#endif
   const int yl = yy - col0;
   if (static_cast<unsigned>(yl) < 8u) {
 #pragma unroll

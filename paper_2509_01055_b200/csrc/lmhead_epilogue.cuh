@@ -17,6 +17,12 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Packed fp32x2 (FFMA2 / FADD2 / FMUL2) in the forward epilogue and the dS
+// pass; 0 = scalar A/B reference build (bitwise-identical results).
+#ifndef TL_EPI_F32X2
+#define TL_EPI_F32X2 1
+#endif
+
 // ------------------------------------------------------------- epilogues --
 __device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
   uint32_t r;
@@ -187,6 +193,7 @@ struct EpiLseStats {
     __half_raw* dst = keep ? p.zout + static_cast<long long>(row) * p.ldz + cb : nullptr;
     float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
     if (nvalid >= 32) {
+#if TL_EPI_F32X2
       // even / odd columns as the two lanes of packed fp32 pairs (FFMA2 /
       // FADD2: same bits as the scalar split accumulators, half the issues)
       uint32_t hq[16];
@@ -205,6 +212,20 @@ struct EpiLseStats {
       s1 = s2.y;
       t0 = t2.x;
       t1 = t2.y;
+#else
+      uint32_t hq[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+        const float u0 = fmaf(v0, kLog2e, -mb), u1 = fmaf(v1, kLog2e, -mb);
+        const float e0 = ex2_ftz(u0), e1 = ex2_ftz(u1);
+        s0 += e0;
+        s1 += e1;
+        t0 = fmaf(e0, v0, t0);
+        t1 = fmaf(e1, v1, t1);
+        hq[j / 2] = pack_f16x2_sat(u0, u1);
+      }
+#endif
       if (keep) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)

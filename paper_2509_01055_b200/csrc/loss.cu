@@ -19,6 +19,8 @@
 //   last-arriving CTA of each level.
 // Every reduction has a fixed shape independent of scheduling, so results are
 // run-to-run deterministic; masked tokens are selected, never multiplied.
+#include <type_traits>
+
 #include "exact_fp64.cuh"
 #include "grpo_token.cuh"
 #include "loss_internal.cuh"
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kUnitThreads) loss_finalize_kernel(const UnitA
 // Streaming kernel: per-token terms (and gradient) over the CTA's contiguous
 // piece of the slot range, one fixed-shape block tree per (piece, trajectory)
 // into the slot of the piece's first unit of that trajectory.
-template <bool kCompute>
+template <bool kCompute, bool kRef = false, int kObj = 0>
 __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel(const UnitArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kPark = 16;  // trajectory pieces parked before a block flush
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel
   const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
   const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
   const float beta = static_cast<float>(a.cfg.kl_beta);
-  const bool has_ref = kCompute && a.cfg.has_ref != 0;
+  constexpr bool has_ref = kCompute && kRef;
   while (s < s_end && b < a.n_traj) {
     const int t0 = cu[b], t1 = cu[b + 1];
     const int kb = b + t0 / kUnit, nb = n_units_of(t1 - t0);
@@ -440,9 +442,13 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel
     const int c1 = rem < nb ? static_cast<int>(rem) : nb;
     const int u0 = min(t1, t0 + c0 * kUnit), u1 = min(t1, t0 + c1 * kUnit);
 
-    // per-thread partials: fp32 sums (a few dozen same-sign terms per thread)
-    // and integer counts; widened to fp64 for the block tree
-    float f_term = 0.f, f_k3 = 0.f, f_ent = 0.f;
+    // per-thread partials: integer counts, and sums in fp64 for the fused
+    // step's reductions (so its report is invariant, to ~1e-15, under
+    // re-packing: data-parallel shards, micro-batches) or fp32 for the
+    // standalone K3 (a few dozen same-sign terms per thread; its result is
+    // deterministic for a given packing, fp32-exact to ~1e-9 across packings)
+    using Acc = std::conditional_t<kCompute, float, double>;
+    Acc f_term = 0, f_k3 = 0, f_ent = 0;
     int n_act = 0, n_clip = 0, n_clamp = 0;
     float adv = 0.f, wt = 0.f;
     if constexpr (kCompute) {
@@ -452,13 +458,12 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel
     auto tok = [&](float x0, float x1, float x2, uint8_t fl, bool act) -> float {
       if (!act) return 0.f;
       if constexpr (kCompute) {
-        const TokTermF o = grpo_token_f32(x0, x1, x2, has_ref && x2 == x2, adv, lo, hi, beta,
-                                          a.cfg.objective);
+        const TokTermB o = grpo_token_t<kRef, kObj>(x0, x1, x2, adv, lo, hi, beta);
         f_term += o.term;
         f_k3 += o.k3;
         n_act += 1;
-        n_clip += (o.flags & kFlagClipped) ? 1 : 0;
-        n_clamp += (o.flags & kFlagClamped) ? 1 : 0;
+        n_clip += o.clipped;
+        n_clamp += o.clamped;
         return o.dterm * wt;
       } else {
         f_term += x0;
@@ -571,7 +576,15 @@ int launch_units(UnitArgs a, long long n_tokens, cudaStream_t st) {
   long long ctas = static_cast<long long>(num_sms()) * kUnitCtasPerSm;
   if (TL_K3_SLOTS_PER_CTA > 0) ctas = (a.n_slots + TL_K3_SLOTS_PER_CTA - 1) / TL_K3_SLOTS_PER_CTA;
   const unsigned grid = static_cast<unsigned>(a.n_slots < ctas ? a.n_slots : ctas);
-  loss_unit_kernel<kCompute><<<grid, kUnitThreads, 0, st>>>(a);
+  if constexpr (kCompute) {  // the config's reference / objective choices as template flags
+    const int v = (a.cfg.has_ref ? 1 : 0) | (a.cfg.objective ? 2 : 0);
+    if (v == 0) loss_unit_kernel<true, false, 0><<<grid, kUnitThreads, 0, st>>>(a);
+    else if (v == 1) loss_unit_kernel<true, true, 0><<<grid, kUnitThreads, 0, st>>>(a);
+    else if (v == 2) loss_unit_kernel<true, false, 1><<<grid, kUnitThreads, 0, st>>>(a);
+    else loss_unit_kernel<true, true, 1><<<grid, kUnitThreads, 0, st>>>(a);
+  } else {
+    loss_unit_kernel<false><<<grid, kUnitThreads, 0, st>>>(a);
+  }
   TL_LAUNCH_CHECK();
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((a.n_groups + kFinGroupsPerCta - 1) / kFinGroupsPerCta);

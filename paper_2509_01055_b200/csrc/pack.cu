@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ int sh_tile;
   __shared__ ScanPair sh_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) sh_tile = atomicAdd(ticket, 1);  // tiles in dispatch order
+  // tiles in dispatch order (a ticket) unless every tile is co-resident
+  if (tid == 0) sh_tile = ticket ? atomicAdd(ticket, 1) : static_cast<int>(blockIdx.x);
   __syncthreads();
   const int tile = sh_tile;
   const int base = tile * kScanTile;
@@ -166,29 +167,44 @@ __global__ void __launch_bounds__(kScanThreads)
     const ScanPair w = lane < kScanThreads / 32 ? warp_tot[lane] : ScanPair{0, 0};
     const ScanPair wi = warp_incl_scan(w);
     if (lane < kScanThreads / 32) warp_tot[lane] = ScanPair{wi.a - w.a, wi.b - w.b};
-    if (lane == kScanThreads / 32 - 1) {
-      // wi = this tile's aggregate: publish, look back, publish the prefix
-      cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
-      ScanPair pre{0, 0};
-      if (tile == 0) {
-        me.store(status_word(kFlagIncl, wi.a, wi.b), cuda::memory_order_release);
-      } else {
-        me.store(status_word(kFlagAgg, wi.a, wi.b), cuda::memory_order_release);
-        for (int j = tile - 1; j >= 0; --j) {
-          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[j]);
-          unsigned long long w;
-          while (((w = st.load(cuda::memory_order_acquire)) >> 62) == 0) {
-          }
-          pre.a += static_cast<int>((w >> 31) & 0x7fffffffull);
-          pre.b += static_cast<int>(w & 0x7fffffffull);
-          if ((w >> 62) == kFlagIncl) break;
+    // this tile's aggregate, broadcast from the last warp-total lane
+    const int agg_a = __shfl_sync(0xffffffffu, wi.a, kScanThreads / 32 - 1);
+    const int agg_b = __shfl_sync(0xffffffffu, wi.b, kScanThreads / 32 - 1);
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[tile]);
+    if (lane == 0)
+      me.store(status_word(tile == 0 ? kFlagIncl : kFlagAgg, agg_a, agg_b),
+               cuda::memory_order_release);
+    // warp-parallel look-back: lane l waits on tile (j - l) of a 32-tile
+    // window; the nearest inclusive prefix ends the walk
+    ScanPair pre{0, 0};
+    for (int j = tile - 1; j >= 0; j -= 32) {
+      const int t = j - lane;
+      unsigned long long sw = status_word(kFlagAgg, 0, 0);
+      if (t >= 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[t]);
+        while (((sw = st.load(cuda::memory_order_acquire)) >> 62) == 0) {
         }
-        me.store(status_word(kFlagIncl, pre.a + wi.a, pre.b + wi.b), cuda::memory_order_release);
       }
+      const unsigned incl_mask = __ballot_sync(0xffffffffu, t >= 0 && (sw >> 62) == kFlagIncl);
+      const int stop = incl_mask ? __ffs(incl_mask) - 1 : 31;  // nearest inclusive lane
+      int va = lane <= stop && t >= 0 ? static_cast<int>((sw >> 31) & 0x7fffffffull) : 0;
+      int vb = lane <= stop && t >= 0 ? static_cast<int>(sw & 0x7fffffffull) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        va += __shfl_xor_sync(0xffffffffu, va, o);
+        vb += __shfl_xor_sync(0xffffffffu, vb, o);
+      }
+      pre.a += va;
+      pre.b += vb;
+      if (incl_mask) break;
+    }
+    if (lane == 0) {
+      if (tile > 0)
+        me.store(status_word(kFlagIncl, pre.a + agg_a, pre.b + agg_b), cuda::memory_order_release);
       sh_prefix = pre;
       if (base + kScanTile >= n_seg) {  // last tile: the batch totals
-        cu_seqlens[n_traj] = pre.a + wi.a;
-        act_off[n_traj] = pre.b + wi.b;
+        cu_seqlens[n_traj] = pre.a + agg_a;
+        act_off[n_traj] = pre.b + agg_b;
       }
     }
   }
@@ -430,9 +446,12 @@ extern "C" int tl_pack_varlen(const int32_t* token_pool, const int32_t* seg_src_
     return TL_OK;
   }
   TL_CUDA_TRY(cudaMemsetAsync(status, 0, (n_tiles + 1) * sizeof(unsigned long long), st));
+  // at most one tile per SM: all tiles are resident at once, so the look-back
+  // cannot wait on an unscheduled tile and blockIdx order is enough
+  const bool coresident = n_tiles <= tl::num_sms();
   tl::pack_scan_kernel<<<n_tiles, tl::kScanThreads, 0, st>>>(
       seg_len, seg_is_action, traj_seg_off, traj_drop, n_traj, n_seg, seg_dst, seg_act, status,
-      ticket, cu_seqlens, act_off);
+      coresident ? nullptr : ticket, cu_seqlens, act_off);
   TL_LAUNCH_CHECK();
   tl::count_launch();
   const long long tiles = (n_tokens + tl::kTilePos - 1) / tl::kTilePos;

@@ -19,7 +19,7 @@ def main(prefix: str):
         cb = d.get("cpu_baseline") or {}
         nan = float("nan")
         rows.append(f"| {c} | {d['config']['workload']} | {d['config']['tokens_per_step']:,} | "
-                    f"{d['config']['action_tokens_per_step']:,} | {d['config'].get('micro_batches', 1)} | "
+                    f"{d['config']['action_tokens_per_step']:,} | {d.get('impl_config', {}).get('micro_batches', d['config'].get('micro_batches', 1))} | "
                     f"{d['ms_per_step']:.1f} | {d['value']:,.0f} | {e.get('value', nan):,.0f} | "
                     f"{r.get('frac', nan):.3f} | {r.get('step_frac', nan):.3f} | "
                     f"{d['clocks'].get('sm_mhz')} | {cb.get('value', nan):.1f} |")
