@@ -267,9 +267,12 @@ def main():
     ap.add_argument("--chunk-rows", type=int, default=None)
     ap.add_argument("--max-mb-tokens", type=int, default=7_000_000,
                     help="largest micro-batch (packed tokens) a rank holds at once")
-    ap.add_argument("--mode", default="store", choices=["store", "pipelined", "recompute"],
+    ap.add_argument("--mode", default="store",
+                    choices=["store", "store-fp16", "pipelined", "recompute"],
                     help="LM-head backward schedule (TL_LMHEAD_* in include/toolloop_b200.h); "
-                         "store is fastest on a power-capped B200 (DESIGN.md §3)")
+                         "store is fastest on a power-capped B200 (DESIGN.md §3) and, without "
+                         "an entropy bonus, runs factored (bf16 q, no dS pass); store-fp16 "
+                         "forces the fp16-logit store + dS pass (TL_LMHEAD_NO_FACTORED)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -364,7 +367,8 @@ def main():
                     "rewards": torch.from_numpy(w.rewards).to(dev),
                     "report": torch.empty(_lib.TL_REPORT_LEN, dtype=torch.float64, device=dev)})
     step = grpo.GRPOStep(H, V, loss_cfg, chunk_rows=args.chunk_rows,
-                         recompute=args.mode == "recompute", pipelined=args.mode == "pipelined")
+                         recompute=args.mode == "recompute", pipelined=args.mode == "pipelined",
+                         factored=args.mode != "store-fp16")
     dhidden_buf = torch.empty((T_max, H), dtype=torch.bfloat16, device=dev)
     dweight = torch.empty((V, H), dtype=torch.float32, device=dev)
     logp_buf = torch.empty(T_max, dtype=torch.float32, device=dev)
@@ -521,7 +525,10 @@ def main():
                                         ("torch.distributed " + dist.get_backend()) if world > 1
                                         else "none"),
                         "chunk_rows": step.last_chunk, "micro_batches": len(mbs),
-                        "lmhead_mode": args.mode},
+                        "lmhead_mode": args.mode + (
+                            " (factored: bf16 q = e^(z - m0), no dS pass)"
+                            if args.mode in ("store", "pipelined") and loss_cfg.entropy_coef == 0
+                            else "")},
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": int(launches),

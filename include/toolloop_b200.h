@@ -253,6 +253,16 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
 /* Debug flag OR-ed into `mode`: run the dW GEMM's partial last wave unsplit
  * (no split-K tail); results agree to fp32 summation order (tests). */
 #define TL_LMHEAD_NO_SPLIT_TAIL 0x200
+/* Debug flag OR-ed into `mode`: keep the fp16-logit store + dS pass even
+ * when the factored store applies.  STORE_LOGITS without the entropy bonus
+ * (entropy_coef == 0) otherwise writes bf16 q = e^(z - m0) against a per-row
+ * anchor m0 and runs dH / dW on q with a per-row scale (dS = alpha_r q plus
+ * one element per row): no elementwise dS pass, same workspace. */
+#define TL_LMHEAD_NO_FACTORED 0x400
+/* Test hook OR-ed into `mode`: the factored store treats every row as out of
+ * its anchor's range and rewrites it on CUDA cores (slow; exercises the
+ * fallback that rows with lse - m0 outside [-45, 80] take). */
+#define TL_LMHEAD_DEBUG_FIXUP 0x800
 /* Workspace for tl_grpo_lmhead_step in `mode` (PIPELINED holds two chunks). */
 size_t tl_lmhead_step_workspace_bytes(int32_t chunk_rows, int32_t hidden, int32_t vocab,
                                       int64_t n_tokens, int32_t n_traj, int32_t n_groups,

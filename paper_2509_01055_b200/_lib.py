@@ -196,12 +196,14 @@ def launch_count() -> int:
     return int(load(False).tl_launch_count())
 
 
-N_PROF = 12
+N_PROF = 13
 LMHEAD_STORE_LOGITS = 0
 LMHEAD_RECOMPUTE = 1
 LMHEAD_STORE_LOGITS_PIPELINED = 2
 LMHEAD_ACCUMULATE_DW = 0x100
 LMHEAD_NO_SPLIT_TAIL = 0x200
+LMHEAD_NO_FACTORED = 0x400
+LMHEAD_DEBUG_FIXUP = 0x800
 
 
 def profile_enable(on: bool = True) -> None:

@@ -47,7 +47,8 @@ std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_pool;
 const char* kProfNames[PROF_N] = {"pack",     "advantage", "loss",     "reduce",
                                   "gather",   "gemm_fwd",  "combine",  "gemm_dsoftmax",
-                                  "gemm_dh",  "gemm_dw",   "gemm_other", "dsoftmax"};
+                                  "gemm_dh",  "gemm_dw",   "gemm_other", "dsoftmax",
+                                  "rescale"};
 
 cudaEvent_t take_event() {
   if (!g_pool.empty()) {

@@ -602,14 +602,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
-// Plain store of the fp32 accumulator as bf16 (optionally with a row remap),
-// used for the dH GEMM (rows scattered back to packed positions) and tests.
+// Plain store of the fp32 accumulator as bf16 (optionally with a row remap
+// and a per-row fp32 scale), used for the dH GEMM (rows scattered back to
+// packed positions; the factored backward's alpha_r) and tests.
 struct EpiStoreBF16 {
   static constexpr bool kSplitTail = false;
   struct Params {
     __nv_bfloat16_raw* out;
-    long long ldo;          // elements
-    const int32_t* row_map; // nullable: out row = row_map[row]
+    long long ldo;            // elements
+    const int32_t* row_map;   // nullable: out row = row_map[row]
+    const float* row_scale;   // nullable: out = row_scale[row] * acc
   };
   struct State {};
   __device__ static void begin_unit(const Params&, const GemmShape&, State&, int, const UnitCoord&) {}
@@ -620,25 +622,28 @@ struct EpiStoreBF16 {
     const bool row_ok = row < s.M;
     long long orow = row;
     if (row_ok && p.row_map) orow = p.row_map[row];
+    const bool scaled = p.row_scale != nullptr;
+    const float sc = row_ok && scaled ? p.row_scale[row] : 1.f;
     tmem_row_slices<BN>(taddr, [&](int c, const uint32_t (&r)[32]) {
       if (!row_ok) return;
       const int cb = col0 + c;
       __nv_bfloat16_raw* dst = p.out + orow * p.ldo + cb;
+      auto val = [&](int j) { return scaled ? __uint_as_float(r[j]) * sc : __uint_as_float(r[j]); };
       if (cb + 32 <= s.N) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
           uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[j + 0]), __uint_as_float(r[j + 1]));
-          v.y = pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-          v.z = pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
-          v.w = pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+          v.x = pack_bf16x2(val(j + 0), val(j + 1));
+          v.y = pack_bf16x2(val(j + 2), val(j + 3));
+          v.z = pack_bf16x2(val(j + 4), val(j + 5));
+          v.w = pack_bf16x2(val(j + 6), val(j + 7));
           *reinterpret_cast<uint4*>(dst + j) = v;
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           if (cb + j < s.N) {
-            const uint32_t b = pack_bf16x2(__uint_as_float(r[j]), 0.f);
+            const uint32_t b = pack_bf16x2(val(j), 0.f);
             dst[j].x = static_cast<unsigned short>(b & 0xFFFFu);
           }
         }

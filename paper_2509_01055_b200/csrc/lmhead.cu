@@ -15,11 +15,16 @@
 //               term / k3 / flags and dLoss/dlogp, dLoss/dent.  In store mode
 //               the epilogue also writes the chunk's logits as fp16
 //               u = (z - m) log2e <= 0 with an int16 offset m per 32 columns
-//               (lmhead_epilogue.cuh).
+//               (lmhead_epilogue.cuh) — or, factored (entropy_coef == 0),
+//               bf16 q = e^(z - m0) with a per-row anchor m0 fixed by the
+//               gather, and the merge turns dS into alpha_r * q.
 //   dsoftmax    (store mode) fp16 u -> bf16 dS in place, HBM-bound
+//   rescale     (factored) h_c *= alpha (dW's B operand); rows outside the
+//               anchor's range rewritten on CUDA cores (never in practice)
 //   recompute   (recompute mode) same GEMM, epilogue writes dS (bf16, [C, V])
 //               dS = g (onehot(y) - p) - c p (z - E_p z),  p = e^(z - lse)
-//   dH GEMM     dhidden[act_idx] = dS W          (A K-major, B = W MN-major)
+//   dH GEMM     dhidden[act_idx] = dS W          (A K-major, B = W MN-major;
+//                                                  factored: alpha (q W))
 //   dW GEMM     dW (+)= dS^T h_c                 (A, B MN-major; fp32 store,
 //               then red.add accumulation across chunks / micro-batches)
 // after all chunks: deterministic trajectory -> group -> batch reductions.
@@ -211,6 +216,112 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t*
   }
 }
 
+__device__ __forceinline__ float dot8_bf16(uint4 a, uint4 b) {
+  const uint32_t x[4] = {a.x, a.y, a.z, a.w}, w[4] = {b.x, b.y, b.z, b.w};
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s = fmaf(__uint_as_float(x[k] << 16), __uint_as_float(w[k] << 16), s);
+    s = fmaf(__uint_as_float(x[k] & 0xFFFF0000u), __uint_as_float(w[k] & 0xFFFF0000u), s);
+  }
+  return s;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Factored store: gather the chunk's action rows (h_c[r] = hidden[idx[r]],
+// y[r] = ids[idx[r]]) and fix each row's anchor m0 before the forward —
+// one warp per row also reads W[y] and takes the fp32 dot product
+// z~_y = h . W[y]; m0 = z~_y + clamp(-logp_old, 0, 40) (20 if logp_old is
+// NaN), i.e. m0 ~ lse when the policy is near the one that sampled the token
+// (lmhead_epilogue.cuh: kQdMin / kQdMax).  z~_y only places the anchor; any
+// value works as long as the row's forward and merge use the same one.
+__global__ void __launch_bounds__(256)
+    gather_anchor_kernel(const uint4* __restrict__ hidden, const uint4* __restrict__ weight,
+                         const int32_t* __restrict__ idx, const int32_t* __restrict__ ids,
+                         const float* __restrict__ logp_old, int rows, int row_vec, int V,
+                         uint4* __restrict__ h_c, int32_t* __restrict__ y_out,
+                         float* __restrict__ anchor) {
+  const int lane = threadIdx.x & 31;
+  const int n_warps = gridDim.x * (blockDim.x / 32);
+  for (int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += n_warps) {
+    const long long p = idx[r];
+    const int y = ids[p];
+    const bool y_ok = static_cast<unsigned>(y) < static_cast<unsigned>(V);
+    const uint4* src = hidden + p * row_vec;
+    const uint4* wy = weight + static_cast<long long>(y_ok ? y : 0) * row_vec;
+    uint4* dst = h_c + static_cast<long long>(r) * row_vec;
+    float acc = 0.f;
+#pragma unroll 2
+    for (int c = lane; c < row_vec; c += 32) {
+      const uint4 h = __ldg(src + c);
+      dst[c] = h;
+      if (y_ok) acc += dot8_bf16(h, __ldg(wy + c));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      y_out[r] = y;
+      const float lo = logp_old[p];
+      anchor[r] = acc + (lo == lo ? fminf(fmaxf(-lo, 0.f), 40.f) : 20.f);
+    }
+  }
+}
+
+// Factored store, rows combine_row listed (lse - m0 outside [kQdMin,
+// kQdMax] with a nonzero gradient; none in practice): recompute the row's
+// logits on CUDA cores (fp32 dot products of the bf16 rows, one warp per
+// vocab entry) and rewrite the row with the anchor m0 = lse: q = p,
+// alpha = -g, A[y] = expm1(logp_y).  Work item = (listed row, 1,024-column
+// block); the list is read on the device, so an empty list costs one launch.
+__global__ void __launch_bounds__(256)
+    fixup_rows_kernel(const int* __restrict__ flagged, const uint4* __restrict__ h_c,
+                      const uint4* __restrict__ weight, int row_vec, int V,
+                      const int32_t* __restrict__ y, const float* __restrict__ lse,
+                      const float* __restrict__ g, float* __restrict__ alpha,
+                      __nv_bfloat16_raw* __restrict__ q, long long ldq) {
+  const int n = flagged[0];
+  if (n == 0) return;
+  constexpr int kCols = 1024;
+  const int nb = (V + kCols - 1) / kCols;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (long long it = blockIdx.x; it < static_cast<long long>(n) * nb; it += gridDim.x) {
+    const int r = flagged[1 + it / nb];
+    const int v0 = static_cast<int>(it % nb) * kCols;
+    const int v1 = min(v0 + kCols, V);
+    const uint4* h = h_c + static_cast<long long>(r) * row_vec;
+    const float l = lse[r];
+    const int yr = y[r];
+    if (v0 == 0 && threadIdx.x == 0) alpha[r] = -g[r];
+    for (int v = v0 + warp; v < v1; v += blockDim.x / 32) {
+      const uint4* w = weight + static_cast<long long>(v) * row_vec;
+      float acc = 0.f;
+      for (int c = lane; c < row_vec; c += 32) acc += dot8_bf16(__ldg(h + c), __ldg(w + c));
+      acc = warp_sum(acc);
+      if (lane == 0) store_bf16(q + static_cast<long long>(r) * ldq + v, v == yr ? expm1f(acc - l) : expf(acc - l));
+    }
+  }
+}
+
+// Factored store: dW's B operand h_c[r] *= alpha_r (bf16, in place).
+__global__ void scale_rows_kernel(uint4* __restrict__ h_c, const float* __restrict__ alpha,
+                                  long long rows, int row_vec) {
+  const long long total = rows * row_vec;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float a = alpha[i / row_vec];
+    uint4 v = h_c[i];
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = pack_bf16x2(__uint_as_float(w[k] << 16) * a, __uint_as_float(w[k] & 0xFFFF0000u) * a);
+    h_c[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
                                   long long n, int32_t* __restrict__ dst) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -373,6 +484,9 @@ struct ChunkWs {
   float* ent;       // [C]
   uint16_t* ds;     // [C, Vld]  fp16 u = (z - m) log2e, then bf16 dS in place
   int16_t* zoff;    // [C, ldo]  int16 slice offsets m of the fp16 u (store mode)
+  float* anc;       // [C]  factored store: anchor m0 per row
+  float* alpha;     // [C]  factored store: dS row scale
+  int* flagged;     // [1 + C] factored store: rows for fixup_rows_kernel
   // step-level
   float* term;      // [T]  (written at action positions only)
   float* k3o;       // [T]
@@ -440,6 +554,9 @@ void carve_chunk(Workspace& w, ChunkWs& c, int C, int H, int V, bool with_bwd) {
   c.ent = w.take<float>(C);
   c.ds = with_bwd ? w.take<uint16_t>(static_cast<size_t>(C) * vld_of(V)) : nullptr;
   c.zoff = with_bwd ? w.take<int16_t>(static_cast<size_t>(C) * ldo_of(V)) : nullptr;
+  c.anc = with_bwd ? w.take<float>(C) : nullptr;
+  c.alpha = with_bwd ? w.take<float>(C) : nullptr;
+  c.flagged = with_bwd ? w.take<int>(C + 1) : nullptr;
   c.sync = w.take<int>(5 * kSyncWaves);
   if (with_bwd) {
     c.tail_part = w.take<float>(static_cast<size_t>(kTailSlots) * kBM * kBNWide);
@@ -513,10 +630,11 @@ GemmShape fwd_shape(int rows, int V, int H, int* sync = nullptr) {
 }
 
 // z = h_c W^T with the online-LSE epilogue, then merge strips.  zout: also
-// keep the chunk's logits in fp16 for the backward (store mode).
+// keep the chunk's logits for the backward (store mode): fp16 u with int16
+// offsets, or (factored) bf16 q against the anchors c.anc.
 int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int H, int V,
-                         CombineArgs ca, cudaStream_t st, __half_raw* zout = nullptr,
-                         long long ldz = 0, int16_t* zoff = nullptr) {
+                         CombineArgs ca, cudaStream_t st, void* zout = nullptr,
+                         long long ldz = 0, int16_t* zoff = nullptr, bool factored = false) {
   CUtensorMap ma, mb;
   if (int e = make_ab_maps(&ma, &mb, c.h, false, rows, H, weight, false, V, H, H, kCG)) return e;
   // fresh wave-lockstep counters for this chunk's GEMMs (fwd / dS / dH / dW)
@@ -527,6 +645,18 @@ int lmhead_forward_chunk(const ChunkWs& c, const uint16_t* weight, int rows, int
   ca.part = c.part;
   ca.n_strips = s.n_strips;
   ca.rows = rows;
+  if (factored) {
+    TL_CUDA_TRY(cudaMemsetAsync(c.flagged, 0, sizeof(int), st));
+    ca.anchor = c.anc;
+    ca.y_row = c.y;
+    ca.alpha_row = c.alpha;
+    ca.qout = static_cast<__nv_bfloat16_raw*>(zout);
+    ca.ldq = ldz;
+    ca.flagged = c.flagged;
+    EpiLseStatsT<true>::Params ep{c.y, c.part, rows, zout, ldz, nullptr, ldo_of(V),
+                                  c.sync + 4 * kSyncWaves, ca, tune::kFwdZStorePolicy, c.anc};
+    return launch_gemm<kCG, false, false, EpiLseStatsT<true>>(ma, mb, s, ep, st, PROF_GEMM_FWD);
+  }
   EpiLseStats::Params ep{c.y, c.part, rows, zout, ldz, zoff, ldo_of(V), c.sync + 4 * kSyncWaves, ca,
                          tune::kFwdZStorePolicy};
   return launch_gemm<kCG, false, false, EpiLseStats>(ma, mb, s, ep, st, PROF_GEMM_FWD);
@@ -607,7 +737,7 @@ extern "C" int tl_gemm_bf16(const uint16_t* A, int32_t a_mn_major, int64_t lda, 
     }
   }
   TL_REQUIRE(!accumulate, TL_ERR_UNSUPPORTED, "accumulate needs fp32 C");
-  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr};
+  EpiStoreBF16::Params ep{static_cast<__nv_bfloat16_raw*>(C), ldc, nullptr, nullptr};
   switch (sel) {
     case 0: return launch_gemm<kCG, false, false, EpiStoreBF16>(ma, mb, s, ep, st);
     case 1: return launch_gemm<kCG, false, true, EpiStoreBF16>(ma, mb, s, ep, st);
@@ -658,7 +788,9 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                                    double* report, int32_t chunk_rows, int32_t mode_flags,
                                    void* workspace, size_t workspace_bytes, tl_stream_t stream) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
-  const int mode = mode_flags & ~(TL_LMHEAD_ACCUMULATE_DW | TL_LMHEAD_NO_SPLIT_TAIL);
+  const int mode =
+      mode_flags & ~(TL_LMHEAD_ACCUMULATE_DW | TL_LMHEAD_NO_SPLIT_TAIL | TL_LMHEAD_NO_FACTORED |
+                     TL_LMHEAD_DEBUG_FIXUP);
   const bool acc_dw = (mode_flags & TL_LMHEAD_ACCUMULATE_DW) != 0;
   const bool no_split_tail = (mode_flags & TL_LMHEAD_NO_SPLIT_TAIL) != 0;
   TL_REQUIRE(mode == TL_LMHEAD_STORE_LOGITS || mode == TL_LMHEAD_RECOMPUTE ||
@@ -702,7 +834,11 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
   }
 
   const bool store = bwd && mode != TL_LMHEAD_RECOMPUTE;
-  const bool pipelined = bwd && mode == TL_LMHEAD_STORE_LOGITS_PIPELINED;
+  // factored store: dS = alpha_r q, no elementwise pass (lmhead_epilogue.cuh)
+  // — exact for dLoss/dz without the entropy term
+  const bool factored = store && ent_grad == 0.f && !(mode_flags & TL_LMHEAD_NO_FACTORED);
+  // the pipelined schedule overlaps the dS pass, which the factored store has not
+  const bool pipelined = bwd && mode == TL_LMHEAD_STORE_LOGITS_PIPELINED && !factored;
   const long long n_chunks = (n_act + chunk_rows - 1) / chunk_rows;
   auto rows_of = [&](long long i) {
     const long long c0 = i * chunk_rows;
@@ -715,7 +851,14 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     const ChunkWs& b = *bufs[i & 1];
     const int rows = rows_of(i);
     const int32_t* ci = act_idx + i * chunk_rows;
-    {
+    if (factored) {
+      ProfScope prof(PROF_GATHER, st);
+      gather_anchor_kernel<<<grid_for(static_cast<long long>(rows) * 32, 256), 256, 0, st>>>(
+          reinterpret_cast<const uint4*>(hidden), reinterpret_cast<const uint4*>(weight), ci,
+          input_ids, logp_old, rows, H / 8, V, reinterpret_cast<uint4*>(b.h), b.y, b.anc);
+      TL_LAUNCH_CHECK();
+      count_launch();
+    } else {
       ProfScope prof(PROF_GATHER, st);
       gather_rows_kernel<<<grid_for((long long)rows * H / 8, 256), 256, 0, st>>>(
           reinterpret_cast<const uint4*>(hidden), ci, rows, H / 8, reinterpret_cast<uint4*>(b.h));
@@ -742,14 +885,29 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     ca.c_row = b.c;
     ca.ez_row = b.ez;
     ca.lse_row = b.lse;
-    return lmhead_forward_chunk(b, weight, rows, H, V, ca, st,
-                                store ? reinterpret_cast<__half_raw*>(b.ds) : nullptr, Vld,
-                                store ? b.zoff : nullptr);
+    ca.force_fixup = (mode_flags & TL_LMHEAD_DEBUG_FIXUP) != 0;
+    return lmhead_forward_chunk(b, weight, rows, H, V, ca, st, store ? b.ds : nullptr, Vld,
+                                store ? b.zoff : nullptr, factored);
   };
   // stage S: dS for the chunk (in place over its fp16 logits, or recomputed)
   auto stage_ds = [&](long long i, cudaStream_t s_ds, int grid) -> int {
     const ChunkWs& b = *bufs[i & 1];
     const int rows = rows_of(i);
+    if (factored) {
+      ProfScope prof(PROF_RESCALE, s_ds);
+      fixup_rows_kernel<<<4 * num_sms(), 256, 0, s_ds>>>(
+          b.flagged, reinterpret_cast<const uint4*>(b.h), reinterpret_cast<const uint4*>(weight),
+          H / 8, V, b.y, b.lse, b.g, b.alpha, reinterpret_cast<__nv_bfloat16_raw*>(b.ds), Vld);
+      TL_LAUNCH_CHECK();
+      count_launch();
+      if (dweight) {
+        scale_rows_kernel<<<grid_for(static_cast<long long>(rows) * H / 8, 256), 256, 0, s_ds>>>(
+            reinterpret_cast<uint4*>(b.h), b.alpha, rows, H / 8);
+        TL_LAUNCH_CHECK();
+        count_launch();
+      }
+      return TL_OK;
+    }
     if (store) {
       ProfScope prof(PROF_DSOFTMAX, s_ds);
       dsoftmax_inplace_kernel<<<grid < rows ? grid : rows, 256, 0, s_ds>>>(
@@ -784,7 +942,8 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
           make_shape(rows, H, V, kBNWide, 1, 1, kCG, tune::kDhPolA, tune::kDhPolB),
           b.sync + 2 * kSyncWaves, tune::kBwdSyncBlocks, tune::kBwdSyncWindow);
       // dhidden rows are written once and not read again in the step
-      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci};
+      EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci,
+                              factored ? b.alpha : nullptr};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
                                                                        PROF_GEMM_DH))
         return e;

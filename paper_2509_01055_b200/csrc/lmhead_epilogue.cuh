@@ -1,7 +1,8 @@
 // LM-head GEMM epilogues (included by lmhead.cu only; see its header for
 // the per-chunk pipeline):
 //   EpiLseStats   forward: per-row online log-sum-exp / E_p z / target logit
-//                 over a vocab strip, fp16 logit stores; the CTA finishing a
+//                 over a vocab strip, logit stores for the backward (fp16 u,
+//                 or bf16 q in the factored mode); the CTA finishing a
 //                 128-row block's last strip merges the strips and runs the
 //                 GRPO surrogate (combine_row).
 //   EpiDSoftmax   recompute mode: dS = dLoss/dz straight from TMEM.
@@ -54,7 +55,40 @@ struct CombineArgs {
   float* g_row;          // [C]
   float* c_row;          // [C]
   float* ez_row;         // [C]
+  // factored store (EpiLseStatsT<true>; nullable anchor = off): per-row
+  // scale alpha, the target column of q rewritten, out-of-range rows listed
+  const float* anchor;         // [C] m0
+  const int32_t* y_row;        // [C] target ids
+  float* alpha_row;            // [C]
+  __nv_bfloat16_raw* qout;     // [C, ldq]
+  long long ldq;
+  int* flagged;                // [1 + C]: count, then row ids
+  int force_fixup;             // test hook (TL_LMHEAD_DEBUG_FIXUP): list every row with g != 0
 };
+
+// Factored backward (entropy_coef == 0).  dS = dLoss/dz = g (onehot(y) - p)
+// is a per-row multiple of q = e^(z - m0) for any per-row anchor m0 fixed
+// before the forward:  dS[r, v] = alpha_r * A[r, v]  with
+//   alpha_r = -g_r e^(m0_r - lse_r),   A[r, v] = q[r, v]  (v != y_r),
+//   A[r, y] = dS_y / alpha_r = expm1(logp_y) e^(lse_r - m0_r).
+// So the forward stores bf16 q, the merge rewrites one element per row
+// (the target) and computes alpha, and the backward needs no elementwise
+// pass: dH = diag(alpha) (A W) (alpha in the dH epilogue) and
+// dW = A^T (diag(alpha) h_c) (h_c scaled in place, a C x H pass).
+// The anchor m0 = z~_y + clamp(-logp_old, 0, 40) (z~_y an fp32 dot product,
+// gather_anchor_kernel) puts m0 near lse, so q ~ p.  d = lse - m0 must stay in
+// [kQdMin, kQdMax]: above, q (<= e^d) and the dH accumulators (sum_v q W <=
+// e^d max|W|) approach fp32 / bf16 range; below, tokens with p > e^(d - 87)
+// would be lost to underflow.  Rows outside (only when the policy moved
+// by e^40+ from logp_old, or logp_old is not a log-prob of this model) are
+// listed and rewritten by fixup_rows_kernel with m0 = lse.
+constexpr float kQdMin = -45.f, kQdMax = 80.f;
+
+__device__ __forceinline__ void store_bf16(__nv_bfloat16_raw* p, float v) {
+  uint32_t b;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(b) : "f"(0.f), "f"(v));
+  p->x = static_cast<unsigned short>(b & 0xFFFFu);
+}
 
 // Merge a row's vocab-strip partials -> lse, logp, entropy; then the GRPO
 // surrogate on logp_new (grpo_token.cuh) -> per-token term / k3 / flags and
@@ -98,9 +132,24 @@ __device__ void combine_row(const CombineArgs& a, int r) {
     a.term[p] = o.term;
     a.k3o[p] = o.k3;
     a.flags[p] = o.flags;
-    a.g_row[r] = -o.dterm * a.traj_w[b];  // loss = -objective
+    const float g = -o.dterm * a.traj_w[b];  // loss = -objective
+    a.g_row[r] = g;
     a.c_row[r] = a.ent_grad;
     a.ez_row[r] = ez;
+    if (a.anchor) {
+      const float d = lse - a.anchor[r];
+      if (g == 0.f) {
+        a.alpha_row[r] = 0.f;  // no gradient: the row's q never matters
+      } else if (d >= kQdMin && d <= kQdMax && !a.force_fixup) {
+        a.alpha_row[r] = -g * expf(-d);
+        // after every strip's q stores of this row (counter + fences)
+        store_bf16(a.qout + static_cast<long long>(r) * a.ldq + a.y_row[r], expm1f(logp) * expf(d));
+      } else {
+        a.alpha_row[r] = 0.f;  // fixup_rows_kernel sets it
+        const int k = atomicAdd(a.flagged, 1);
+        a.flagged[1 + k] = r;
+      }
+    }
   }
 }
 
@@ -119,28 +168,38 @@ __device__ void combine_row(const CombineArgs& a, int r) {
 // relative at |z| >= 16 (per-row dH errors up to 6.6x on p_y -> 1 rows,
 // tests/test_lmhead_bwd_fullshape_gpu.py).  The quantised m also drives the
 // log-sum-exp itself (any offset >= the max works).
+//
+// kFactored (entropy_coef == 0, see combine_row): the stores are bf16
+// q = e^(z - m0) = 2^u * f with the row's fixed anchor m0 and the per-row
+// factor f = 2^((m - m0) log2e), updated only when the running max m moves:
+// one FMUL per logit, no offsets; the log-sum-exp itself is unchanged, so
+// logp / entropy / the report are bitwise those of the fp16-u store.
 constexpr float kOffScale = 128.f;             // offset units: 1/128
 constexpr float kMaxOff = 32767.f / kOffScale;  // |m| cap (|z| beyond ~256: unsupported)
 
-struct EpiLseStats {
+template <bool kFactored>
+struct EpiLseStatsT {
   static constexpr bool kSplitTail = false;
   struct Params {
     const int32_t* targets;  // [C] target id of each chunk row
     float4* part;            // [n_strips, C]: (max, sum e, sum e z, z_target)
     int rows;                // C (partials row stride)
-    __half_raw* zout;        // optional fp16 u = (z - m) log2e store [C, ldz] (backward input)
+    void* zout;              // optional backward input [C, ldz]: fp16 u = (z - m) log2e, or
+                             // (kFactored) bf16 q = e^(z - m0)
     long long ldz;
     int16_t* zoff;           // [C, ldo] slice offsets m (8 per 256-column tile), with zout
     long long ldo;
     int* tile_ctr;           // [ceil(C/128)] strips finished per 128-row block (zeroed)
     CombineArgs ca;          // last-strip fixup: merge + surrogate for the block's rows
     int z_policy;            // make_policy() kind of the fp16 stores
+    const float* anchor;     // kFactored: [C] m0 per row
   };
   struct State {
     float m, s, t, zy;
     int y;
     uint64_t zpol;
     uint64_t olo, ohi;  // the tile's 8 slice offsets (int16), shifted in slice by slice
+    float a, f;         // kFactored: m0 log2e, 2^(m log2e - a)
   };
   __device__ static void begin_unit(const Params& p, const GemmShape& sh, State& st, int row,
                                     const UnitCoord&) {
@@ -151,6 +210,8 @@ struct EpiLseStats {
     st.y = row < sh.M ? p.targets[row] : -1;
     st.zpol = make_policy(p.z_policy);
     st.olo = st.ohi = 0;
+    st.a = kFactored && row < sh.M ? p.anchor[row] * kLog2e : 0.f;
+    st.f = 0.f;
   }
   // One 32-column slice of the row: running max rescale, then sum e and
   // sum e*z with e = 2^u, u = z*log2e - m*log2e, and (store mode) fp16 u.
@@ -187,10 +248,14 @@ struct EpiLseStats {
       st.s *= f;
       st.t *= f;
       st.m = mq;
+      // exponent capped: rows that far above their anchor are rewritten by
+      // the fixup (combine_row), the cap only keeps q finite meanwhile
+      if constexpr (kFactored) st.f = ex2_ftz(fminf(fmaf(mq, kLog2e, -st.a), 126.f));
     }
     const float mb = st.m * kLog2e;
     const bool keep = p.zout != nullptr && row < sh.M;
-    __half_raw* dst = keep ? p.zout + static_cast<long long>(row) * p.ldz + cb : nullptr;
+    uint16_t* dst = keep ? static_cast<uint16_t*>(p.zout) + static_cast<long long>(row) * p.ldz + cb
+                         : nullptr;
     float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
     if (nvalid >= 32) {
 #if TL_EPI_F32X2
@@ -206,7 +271,12 @@ struct EpiLseStats {
         const float2 e = make_float2(ex2_ftz(u.x), ex2_ftz(u.y));
         s2 = fadd2(s2, e);
         t2 = ffma2(e, v, t2);
-        hq[j / 2] = pack_f16x2_sat(u.x, u.y);
+        if constexpr (kFactored) {
+          const float2 q = fmul2(e, make_float2(st.f, st.f));
+          hq[j / 2] = pack_bf16x2(q.x, q.y);
+        } else {
+          hq[j / 2] = pack_f16x2_sat(u.x, u.y);
+        }
       }
       s0 = s2.x;
       s1 = s2.y;
@@ -223,7 +293,8 @@ struct EpiLseStats {
         s1 += e1;
         t0 = fmaf(e0, v0, t0);
         t1 = fmaf(e1, v1, t1);
-        hq[j / 2] = pack_f16x2_sat(u0, u1);
+        if constexpr (kFactored) hq[j / 2] = pack_bf16x2(e0 * st.f, e1 * st.f);
+        else hq[j / 2] = pack_f16x2_sat(u0, u1);
       }
 #endif
       if (keep) {
@@ -241,12 +312,13 @@ struct EpiLseStats {
         s0 += e;
         t0 = fmaf(e, v, t0);
         if (keep && j < nvalid)
-          dst[j].x = static_cast<unsigned short>(pack_f16x2_sat(u, 0.f) & 0xFFFFu);
+          dst[j] = static_cast<unsigned short>(
+              (kFactored ? pack_bf16x2(e * st.f, 0.f) : pack_f16x2_sat(u, 0.f)) & 0xFFFFu);
       }
     }
     st.s += s0 + s1;
     st.t += t0 + t1;
-    if (p.zout) {  // this slice's offset m into the tile's 8-slot shift register
+    if (!kFactored && p.zout) {  // this slice's offset m into the tile's 8-slot shift register
       const uint64_t m16 =
           static_cast<uint16_t>(static_cast<int16_t>(fmaxf(st.m, -kMaxOff) * kOffScale));
       st.olo = (st.olo >> 16) | (st.ohi << 48);
@@ -272,7 +344,7 @@ struct EpiLseStats {
       slice(p, sh, st, row, col0 + c + 32, rb);
       if (more) tmem_ld_wait_regs(ra);
     }
-    if (p.zout && row < sh.M)
+    if (!kFactored && p.zout && row < sh.M)
       st_v4_hint(p.zoff + static_cast<long long>(row) * p.ldo + col0 / 32,
                  make_uint4(static_cast<uint32_t>(st.olo), static_cast<uint32_t>(st.olo >> 32),
                             static_cast<uint32_t>(st.ohi), static_cast<uint32_t>(st.ohi >> 32)),
@@ -305,6 +377,7 @@ struct EpiLseStats {
     }
   }
 };
+using EpiLseStats = EpiLseStatsT<false>;
 
 // dS = dLoss/dz (bf16) from recomputed logits.
 struct EpiDSoftmax {

@@ -80,6 +80,7 @@ enum ProfCat {
   PROF_GEMM_DW,
   PROF_GEMM_OTHER,
   PROF_DSOFTMAX,
+  PROF_RESCALE,
   PROF_N
 };
 struct ProfScope {

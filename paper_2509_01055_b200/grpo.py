@@ -175,7 +175,8 @@ class GRPOStep:
 
     def __init__(self, hidden_dim: int, vocab: int, cfg: LossConfig | None = None,
                  chunk_rows: int | None = None, recompute: bool = False,
-                 pipelined: bool = False, split_tail: bool = True):
+                 pipelined: bool = False, split_tail: bool = True, factored: bool = True,
+                 debug_fixup: bool = False):
         """recompute=False keeps each chunk's logits in fp16 for the backward
         (6*T*H*V FLOPs); True recomputes them in a second GEMM (8*T*H*V) so no
         logit ever leaves TMEM.  pipelined=True (store mode) double-buffers the
@@ -183,7 +184,11 @@ class GRPOStep:
         forward GEMM (include/toolloop_b200.h, TL_LMHEAD_*); bitwise equal to
         the serial schedule but measured 3 % slower at C2 on a power-capped
         B200 (the GEMM slows by as much as the pass it hides), so off by
-        default."""
+        default.  factored=True (store mode, entropy_coef == 0): the forward
+        stores bf16 q = e^(z - m0) against a per-row anchor and dS = alpha_r q
+        reaches the dH / dW GEMMs without an elementwise pass (False:
+        TL_LMHEAD_NO_FACTORED); debug_fixup (tests) routes every row through
+        the out-of-range fallback."""
         self.H = int(hidden_dim)
         self.V = int(vocab)
         self.cfg = cfg or LossConfig()
@@ -196,6 +201,10 @@ class GRPOStep:
             self.mode = _lib.LMHEAD_STORE_LOGITS
         # split_tail=False (tests): the dW GEMM's partial last wave runs unsplit
         self.flags = 0 if split_tail else _lib.LMHEAD_NO_SPLIT_TAIL
+        if not factored:
+            self.flags |= _lib.LMHEAD_NO_FACTORED
+        if debug_fixup:
+            self.flags |= _lib.LMHEAD_DEBUG_FIXUP
         self._ws = _Workspace()
         self.last_chunk = None  # chunk rows used by the latest call
 

@@ -10,6 +10,10 @@ the clipped-surrogate restatement (oracle.grpo_oracle.term_and_grad), so the
 GPU forward, the fused surrogate epilogue, the dS pass and the dH / dW GEMMs
 are all checked.
 
+Backward modes: "store" (entropy bonus on: fp16 logits + dS pass),
+"factored" (no entropy bonus: bf16 q against a per-row anchor, no dS pass),
+"recompute" (second GEMM writes dS).
+
 Two logit scales:
   init       W ~ N(0, 0.02): logit std ~1.2 (the bench's synthetic weights)
   realistic  W std so that max |z| ~ 30 (trained LM heads reach |z| 20-40),
@@ -85,7 +89,7 @@ def _case(shape, scale, seed=0):
     return cfg, wl, packed, h, W
 
 
-@pytest.mark.parametrize("mode", ["store", "recompute"])
+@pytest.mark.parametrize("mode", ["store", "factored", "recompute"])
 @pytest.mark.parametrize("scale", ["init", "realistic"])
 @pytest.mark.parametrize("shape", ["c2", "c5"])
 def test_backward_full_shape_vs_oracle(shape, scale, mode):
@@ -99,7 +103,10 @@ def test_backward_full_shape_vs_oracle(shape, scale, mode):
     go = wl.group_off
     n_groups = len(go) - 1
     token_mean = cfg.loss_agg == L.AGG_TOKEN_MEAN
-    beta, coef = 0.04, 0.01
+    # "factored": no entropy bonus, so the store mode keeps bf16 q = e^(z - m0)
+    # and skips the dS pass (tests/test_factored_gpu.py); "store" keeps the
+    # fp16 logits + dS pass (entropy bonus on)
+    beta, coef = 0.04, (0.0 if mode == "factored" else 0.01)
     lc = L.LossConfig(epsilon_clip=0.2, kl_beta=beta, entropy_coef=coef, loss_agg=cfg.loss_agg)
 
     # behaviour / reference policy log-probs near the oracle's current logp
