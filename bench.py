@@ -41,7 +41,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "masked GRPO-step tokens/sec (pack+adv+logprob+loss) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "tokens/s"
 # ncu DRAM bytes of one C2 chunk (tools/profile_summary.py) for roofline.traffic
-TRAFFIC_JSON = "r2c_gemm_traffic.json"
+TRAFFIC_JSON = "r2d_gemm_traffic.json"
 
 
 def _peaks():
@@ -498,7 +498,10 @@ def main():
         traffic = per_chunk * 1e9 * n_act / tj["chunk_rows"]
         traffic_note = (f"bytes/step = ncu --set full DRAM read+write of the fwd/dH/dW GEMM launches "
                         f"of one {tj['chunk_rows']}-row chunk ({per_chunk:.1f} GB, {tp.name}) x chunks/step; "
-                        f"per chunk each GEMM must read W (1.09 GB) and h_c or dS (0.27 / 11.5 GB) once")
+                        f"reading every operand once would be 39.7 GB per chunk, but an output-stationary "
+                        f"tile schedule on 74 CTA pairs re-reads W once per dH wave and h_c once per dW "
+                        f"wave (TMEM holds one 256x512 fp32 tile per pair): 72.2 GB per chunk is "
+                        f"compulsory for it (DESIGN.md section 3)")
     if gemm_ms > 0:
         ach = flops_alg / (gemm_ms / 1e3) / 1e12
         roofline = {

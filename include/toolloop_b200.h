@@ -214,9 +214,11 @@ int tl_loss_f32(const float* logp_new, const float* logp_old, const float* logp_
  * rows.  The forward sweeps the vocabulary in 256-wide tiles with an online
  * log-sum-exp, so the log-probs never need [T, V] logits.  The backward
  * needs p = softmax(z) once the final LSE is known: STORE_LOGITS keeps ONE
- * chunk's logits ([chunk_rows, V] fp16, 46 GB at 4 x 37,888 rows and
- * V = 152,064) and reuses that buffer for bf16 dS; RECOMPUTE keeps no
- * logits and recomputes them in a second GEMM.  [T, V] is never allocated.
+ * chunk's [chunk_rows, V] 2-byte buffer (46 GB at 4 x 37,888 rows and
+ * V = 152,064) — bf16 q = e^(z - m0) that the dH / dW GEMMs read directly
+ * (factored, no entropy bonus), or fp16 logits turned into bf16 dS in place
+ * (entropy bonus on); RECOMPUTE keeps no logits and recomputes them in a
+ * second GEMM.  [T, V] is never allocated: one chunk at a time.
  * ---------------------------------------------------------------------- */
 /* Workspace of tl_grpo_lmhead_step in the serial modes (STORE_LOGITS,
  * RECOMPUTE) with the backward: one chunk's [chunk_rows, V] dS buffer, the
@@ -234,10 +236,14 @@ int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight, const int
                        float* logp, float* entropy, float* lse, int32_t chunk_rows,
                        void* workspace, size_t workspace_bytes, tl_stream_t stream);
 /* Backward modes of tl_grpo_lmhead_step.
- *  STORE_LOGITS: the forward epilogue also writes the chunk's logits as fp16
- *    into the [chunk_rows, V] workspace; an elementwise pass turns them into
- *    bf16 dS in place (6*T*H*V issued FLOPs; [T, V] is never allocated — only
- *    one chunk at a time).
+ *  STORE_LOGITS: the forward epilogue also writes the chunk's logits into the
+ *    [chunk_rows, V] workspace (6*T*H*V issued FLOPs; [T, V] is never
+ *    allocated — only one chunk at a time).  Without the entropy bonus
+ *    (entropy_coef == 0) dS = alpha_r * q row by row, so the forward stores
+ *    bf16 q = e^(z - m0) against a per-row anchor m0 and the dH / dW GEMMs
+ *    read q with alpha folded into the dH epilogue and into h_c ("factored",
+ *    no elementwise pass); with the bonus it stores fp16 logits and an
+ *    elementwise pass turns them into bf16 dS in place.
  *  RECOMPUTE: the backward recomputes the logits with a second GEMM whose
  *    epilogue writes dS (8*T*H*V issued FLOPs; no logits ever leave TMEM). */
 #define TL_LMHEAD_STORE_LOGITS 0

@@ -30,7 +30,7 @@ def main(prefix: str):
             "Fraction = algorithmic 6*T_act*H*V over the GEMMs' event time (frac) / over the whole step "
             "(step frac), against MEASURED_PEAKS.json bf16_tflops_sustained.  C3/C4 hold more activations "
             "than HBM, so each step runs as micro-batches of whole groups (global normalisers, dW accumulated, "
-            "reports combined).  C3 is run with --no-e2e.  C1 (H 896) spends 11 % of its step in the 4 B/logit dS pass.  Boxes "
+            "reports combined).  C3 is run with --no-e2e.  C1 (H 896, V 32k, 18.6 k action rows: one small chunk) is launch- and tail-bound.  Boxes "
             "differ by ~3 %.  Raw JSON lines: " + f"{prefix}_bench_cN.json.log.\n\n" + hdr + "\n" +
             "\n".join(rows) + "\n")
     (PROF / f"{prefix}_configs.md").write_text(text)

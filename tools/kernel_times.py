@@ -1,7 +1,7 @@
 """Per-kernel device durations (CUPTI via torch.profiler, kernels running
 back to back as in production — not serialised like ncu) of the memory-bound
-path: K1 pack, K2 advantages, K3 loss.  L2 is flushed (256 MB write) before
-every iteration.  Prints one JSON line: {op: {kernel name: {"us": median,
+path: K1 pack, K2 advantages, K3 loss.  L2 is flushed before every iteration (256 MB write, then a
+256 MB read so the kernels start on a clean L2).  Prints one JSON line: {op: {kernel name: {"us": median,
 "n": launches per iteration}, "_span_us": first kernel start -> last end}}.
 
     python tools/kernel_times.py [c2]
@@ -24,12 +24,14 @@ from paper_2509_01055_b200.synthetic import CONFIGS, make_workload  # noqa: E402
 
 def kernel_spans(fn, iters=10):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
     fn()
     torch.cuda.synchronize()
     per = defaultdict(list)
     spans = []
     for _ in range(iters):
-        flush.fill_(1)
+        flush.fill_(1)       # > L2 (the bench rule) ...
+        flush_rd.sum()       # ... then a read, so the dirty lines are written back before timing
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             fn()

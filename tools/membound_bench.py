@@ -21,6 +21,20 @@ from paper_2509_01055_b200.synthetic import CONFIGS, make_workload  # noqa: E402
 PEAK = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
     if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6650.0
 FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+FLUSH_RD = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB
+
+
+def flush_l2():
+    """Write a buffer larger than the 126 MB L2 (the bench rule), then read
+    another one: the write's dirty lines are written back during the read,
+    so the timed kernels start on a clean L2 (with the write alone they pay
+    up to ~126 MB of write-backs of the flush buffer, as much DRAM traffic
+    as K3 itself).  MEMBOUND_FLUSH=write keeps the write-only flush."""
+    import os
+
+    FLUSH.fill_(1)
+    if os.environ.get("MEMBOUND_FLUSH", "write+read") != "write":
+        FLUSH_RD.sum()
 
 
 def timed(fn, iters=None):
@@ -29,7 +43,7 @@ def timed(fn, iters=None):
     iters = int(os.environ.get("MEMBOUND_ITERS", "10")) if iters is None else iters
     ts = []
     for _ in range(iters + 2):
-        FLUSH.fill_(1)
+        flush_l2()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
@@ -47,7 +61,7 @@ def device_ms(fn, cat, iters=5):
     back and the events measure device time, not host submission latency."""
     ts = []
     for _ in range(iters):
-        FLUSH.fill_(1)
+        flush_l2()
         torch.cuda.synchronize()
         torch.cuda._sleep(2_000_000)
         _lib.profile_enable(True)
@@ -105,16 +119,25 @@ def main():
     sub = packing.PackedBatch(packed.input_ids, packed.loss_mask, packed.position_ids,
                               packed.traj_of_token, packed.cu_seqlens, packed.act_off, idx,
                               packed.n_traj, packed.n_tokens, n)
-    step = grpo.GRPOStep(H, V, c, chunk_rows=n)
-    step(sub, go, rw, hidden, weight, lold, lref)
-    torch.cuda.synchronize()
-    _lib.profile_enable(True)
-    step(sub, go, rw, hidden, weight, lold, lref)
-    torch.cuda.synchronize()
-    prof = _lib.profile_read()
-    _lib.profile_enable(False)
-    res["dsoftmax (K5, one chunk)"] = (prof["dsoftmax"][0], 4 * n * V)
-    res["gather action rows (one chunk)"] = (prof["gather"][0], 4 * n * H + 8 * n)
+    def chunk_prof(factored):
+        step = grpo.GRPOStep(H, V, c, chunk_rows=n, factored=factored)
+        step(sub, go, rw, hidden, weight, lold, lref)
+        torch.cuda.synchronize()
+        _lib.profile_enable(True)
+        step(sub, go, rw, hidden, weight, lold, lref)
+        torch.cuda.synchronize()
+        prof = _lib.profile_read()
+        _lib.profile_enable(False)
+        return prof
+
+    prof = chunk_prof(False)  # fp16-logit store: the dS pass (kept for the entropy bonus)
+    res["dsoftmax (K5, one chunk, fp16 store)"] = (prof["dsoftmax"][0], 4 * n * V)
+    res["gather action rows (one chunk, fp16 store)"] = (prof["gather"][0], 4 * n * H + 8 * n)
+    prof = chunk_prof(True)  # factored store (default without the entropy bonus)
+    # gather + anchor: hidden rows and W[y] rows read, h_c written, ids / anchors
+    res["gather + anchor (one chunk, factored)"] = (prof["gather"][0], 6 * n * H + 16 * n)
+    # fixup (empty list) + h_c *= alpha in place
+    res["rescale (one chunk, factored)"] = (prof["rescale"][0], 4 * n * H + 4 * n)
     for k, (ms, by) in res.items():
         gbs = by / (ms / 1e3) / 1e9
         out[k] = {"ms": round(ms, 4), "bytes": int(by), "GB_s": round(gbs, 1),

@@ -30,7 +30,7 @@ def role(name):
     for k, v in ROLE.items():
         if "gemm_sm100" in name and k in name:
             return v
-    for k in ("dsoftmax", "gather_rows", "pack_scatter", "pack_scan", "group_adv",
+    for k in ("dsoftmax", "gather_rows", "gather_anchor", "fixup_rows", "scale_rows", "pack_scatter", "pack_scan", "group_adv",
               "loss_unit_kernel<true>", "loss_unit_kernel<false>", "loss_finalize"):
         if k in name:
             return k

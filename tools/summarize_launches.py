@@ -8,10 +8,11 @@ from collections import defaultdict
 
 
 def short(name: str) -> str:
-    m = re.match(r"void (tl::)?gemm_sm100_kernel<(\d+), \d+, \d+, (\w+), (\w+), (?:tl::)?(?:\(anonymous namespace\)::|<unnamed>::)?(\w+)>", name)
+    m = re.match(r"void (tl::)?gemm_sm100_kernel<(\d+), \d+, \d+, (\w+), (\w+), (?:tl::)?(?:\(anonymous namespace\)::|<unnamed>::)?(\w+(?:<\d+>)?)>", name)
     if m:
-        role = {"EpiLseStats": "K4 fwd", "EpiStoreF32": "K5 dW", "EpiStoreBF16": "K5 dH",
-                "EpiDSoftmax": "dS recompute"}.get(m.group(5), m.group(5))
+        role = {"EpiLseStats": "K4 fwd", "EpiLseStatsT<0>": "K4 fwd (fp16 store / forward only)",
+                "EpiLseStatsT<1>": "K4 fwd (factored store)", "EpiStoreF32": "K5 dW",
+                "EpiStoreBF16": "K5 dH", "EpiDSoftmax": "dS recompute"}.get(m.group(5), m.group(5))
         return f"gemm_sm100_kernel<{m.group(2)},..,{m.group(5)}> ({role})"
     return name.split("(")[0][:90]
 
