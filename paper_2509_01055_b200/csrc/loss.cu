@@ -201,12 +201,7 @@ __global__ void ratio64_kernel(const double* __restrict__ a, const double* __res
 // writes the report.  Every sum has a fixed shape (a function of the sizes
 // only), so results are bitwise run-to-run deterministic whichever CTA
 // arrives last; masked-out tokens are selected, never multiplied.
-// Walker of the streaming kernel: 1 = one warp per contiguous slot range
-// (units of 1,024 tokens), 0 = one CTA (units of 2,048 tokens).
-#ifndef TL_K3_WALK
-#define TL_K3_WALK 1
-#endif
-constexpr int kUnit = TL_K3_WALK == 1 ? 1024 : 2048;
+constexpr int kUnit = 2048;
 constexpr int kUnitThreads = 256;
 constexpr int kUnitCtasPerSm = 4;  // resident CTAs per SM (<= 64 registers)
 constexpr int kRedV = 6;  // term, k3, n_act, clipped, clamps, entropy
@@ -390,71 +385,44 @@ __global__ void __launch_bounds__(kUnitThreads) loss_finalize_kernel(const UnitA
   *a.ctr = 0;  // ready for the next launch
 }
 
-// Streaming kernel: per-token terms (and gradient) over a contiguous piece of
-// the slot range, one fixed-shape tree per (piece, trajectory) into the slot
-// of the piece's first unit of that trajectory.  The walker that owns a piece
-// is a warp (kWarp, TL_K3_WALK = 1: 32 lanes, 32 tokens per lane per 1,024-
-// token unit, the partial reduced with shuffles and written straight to its
-// slot) or the whole CTA (TL_K3_WALK = 0: 256 threads, warp partials parked in
-// shared memory and summed in warp order every 16 pieces).  The warp walker
-// has ~5x fewer (walker, trajectory) pieces per token to reduce and no block
-// barriers; both are deterministic (every sum has a fixed shape).
+// Streaming kernel: per-token terms (and gradient) over the CTA's contiguous
+// piece of the slot range, one fixed-shape block tree per (piece, trajectory)
+// into the slot of the piece's first unit of that trajectory.
 template <bool kCompute, bool kRef = false, int kObj = 0>
 __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel(const UnitArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  constexpr bool kWarp = TL_K3_WALK == 1;
-  constexpr int NT = kWarp ? 32 : kUnitThreads;  // threads of one walker
-  constexpr int kPark = 16;  // (CTA walker) trajectory pieces parked before a block flush
+  constexpr int kPark = 16;  // trajectory pieces parked before a block flush
   constexpr int kWarps = kUnitThreads / 32;
-  __shared__ double park[kWarp ? 1 : kPark][kWarps][kRedV];
+  __shared__ double park[kPark][kWarps][kRedV];
   __shared__ int park_slot[kPark], park_units[kPark];
   int n_park = 0;
-  const int gt = kWarp ? static_cast<int>(threadIdx.x & 31) : static_cast<int>(threadIdx.x);
   // sum the parked warp partials in warp order -> the slot of the piece's
   // first unit of each trajectory, zeros in the slots of the folded units
   auto flush = [&]() {
-    if constexpr (!kWarp) {
-      __syncthreads();
-      for (int j = threadIdx.x; j < n_park; j += kUnitThreads) {
-        double* uo = a.unit_out + static_cast<long long>(park_slot[j]) * 8;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n_park; j += kUnitThreads) {
+      double* uo = a.unit_out + static_cast<long long>(park_slot[j]) * 8;
 #pragma unroll
-        for (int i = 0; i < kRedV; ++i) {
-          double x = 0;
+      for (int i = 0; i < kRedV; ++i) {
+        double x = 0;
 #pragma unroll
-          for (int w = 0; w < kWarps; ++w) x += park[j][w][i];
-          uo[i] = x;
-        }
-        for (int c = 1; c < park_units[j]; ++c)
-#pragma unroll
-          for (int i = 0; i < kRedV; ++i) uo[c * 8 + i] = 0.0;
+        for (int w = 0; w < kWarps; ++w) x += park[j][w][i];
+        uo[i] = x;
       }
-      __syncthreads();
-      n_park = 0;
+      for (int c = 1; c < park_units[j]; ++c)
+#pragma unroll
+        for (int i = 0; i < kRedV; ++i) uo[c * 8 + i] = 0.0;
     }
+    __syncthreads();
+    n_park = 0;
   };
   const int32_t* cu = a.cu;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.ctr = 0;  // finalize's arrival counter
-  // this walker's contiguous piece of the slot range
-  const long long n_walk = kWarp ? static_cast<long long>(gridDim.x) * kWarps : gridDim.x;
-  const long long wid = kWarp ? static_cast<long long>(blockIdx.x) * kWarps + (threadIdx.x >> 5)
-                              : blockIdx.x;
-  const long long s_begin = a.n_slots * wid / n_walk;
-  const long long s_end = a.n_slots * (wid + 1) / n_walk;
+  // this CTA's contiguous piece of the slot range
+  const long long s_begin = a.n_slots * blockIdx.x / gridDim.x;
+  const long long s_end = a.n_slots * (blockIdx.x + 1) / gridDim.x;
   if (s_begin >= s_end) return;
-  int b;
-  if constexpr (kWarp) {  // 32-ary warp search: last b with key(b) <= s_begin
-    int lo = 0, hi = a.n_traj;
-    while (hi - lo > 1) {
-      const int step = (hi - lo + 31) / 32;
-      const int idx = lo + gt * step;
-      const unsigned m = __ballot_sync(0xffffffffu, idx < hi && unit_key(cu, idx) <= s_begin);
-      lo += (__popc(m) - 1) * step;
-      hi = min(hi, lo + step);
-    }
-    b = lo;
-  } else {
-    b = block_find_key(a.n_traj, s_begin, [cu](int i) { return unit_key(cu, i); });
-  }
+  int b = block_find_key(a.n_traj, s_begin, [cu](int i) { return unit_key(cu, i); });
   long long s = s_begin;
   const float lo = static_cast<float>(1.0 - a.cfg.eps_low);
   const float hi = static_cast<float>(1.0 + a.cfg.eps_high);
@@ -523,13 +491,13 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel
     // flight instead of one dependent mask -> log-prob round trip per quad.
     const int b0 = (u0 + 3) & ~3, b1 = u1 & ~3;
     if (!a.vec_ok || b0 >= b1) {
-      for (int t = u0 + gt; t < u1; t += NT) scalar(t);
+      for (int t = u0 + threadIdx.x; t < u1; t += kUnitThreads) scalar(t);
     } else {
-      if (u0 + gt < b0) scalar(u0 + gt);
-      if (b1 + gt < u1) scalar(b1 + gt);
+      if (u0 + static_cast<int>(threadIdx.x) < b0) scalar(u0 + threadIdx.x);
+      if (b1 + static_cast<int>(threadIdx.x) < u1) scalar(b1 + threadIdx.x);
       constexpr int kBatch = 2;
-      constexpr int kStride = 4 * NT;
-      for (int base = b0 + 4 * gt; base < b1; base += kBatch * kStride) {
+      constexpr int kStride = 4 * kUnitThreads;
+      for (int base = b0 + 4 * threadIdx.x; base < b1; base += kBatch * kStride) {
         uchar4 m[kBatch];
         float4 x0[kBatch], x1[kBatch], x2[kBatch];
         uchar4 fl[kBatch];
@@ -571,34 +539,20 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitCtasPerSm) loss_unit_kernel
         }
       }
     }
-    // warp partial (fixed shuffle tree)
+    // warp partial (fixed shuffle tree) parked per (trajectory of the piece,
+    // warp); no block barrier per trajectory — warps run through the piece
+    // independently and the block combines the parked partials in warp order
     double v[kRedV] = {f_term, f_k3, static_cast<double>(n_act), static_cast<double>(n_clip),
                        static_cast<double>(n_clamp), f_ent};
     warp_sum(v);
-    if constexpr (kWarp) {
-      // the walker is this warp: its partial goes straight to the slot of
-      // the piece's first unit, zeros to the folded units' slots
-      double* uo = a.unit_out + (kb + c0) * 8LL;
-      if (gt < kRedV) {
-        double x = v[0];
+    if ((threadIdx.x & 31) == 0)
 #pragma unroll
-        for (int i = 1; i < kRedV; ++i) x = gt == i ? v[i] : x;
-        uo[gt] = x;
-      }
-      for (int k = gt; k < (c1 - c0 - 1) * kRedV; k += 32) uo[(1 + k / kRedV) * 8 + k % kRedV] = 0.0;
-    } else {
-      // parked per (trajectory of the piece, warp); no block barrier per
-      // trajectory — warps run through the piece independently and the block
-      // combines the parked partials in warp order
-      if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int i = 0; i < kRedV; ++i) park[n_park][threadIdx.x >> 5][i] = v[i];
-      if (threadIdx.x == 0) {
-        park_slot[n_park] = kb + c0;
-        park_units[n_park] = c1 - c0;
-      }
-      if (++n_park == kPark) flush();
+      for (int i = 0; i < kRedV; ++i) park[n_park][threadIdx.x >> 5][i] = v[i];
+    if (threadIdx.x == 0) {
+      park_slot[n_park] = kb + c0;
+      park_units[n_park] = c1 - c0;
     }
+    if (++n_park == kPark) flush();
     s = kb + c1;
     ++b;
   }
