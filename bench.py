@@ -267,6 +267,10 @@ def main():
     ap.add_argument("--chunk-rows", type=int, default=None)
     ap.add_argument("--max-mb-tokens", type=int, default=7_000_000,
                     help="largest micro-batch (packed tokens) a rank holds at once")
+    ap.add_argument("--n2-overlap", type=int, default=0, metavar="SMS",
+                    help="N > 1 with NCCL: run the dW all-reduce on a side stream beside the "
+                         "last chunk's dH GEMM, which leaves SMS SMs free for it (0: after the "
+                         "step; DESIGN.md section 6)")
     ap.add_argument("--mode", default="store",
                     choices=["store", "store-fp16", "pipelined", "recompute"],
                     help="LM-head backward schedule (TL_LMHEAD_* in include/toolloop_b200.h); "
@@ -374,6 +378,9 @@ def main():
     logp_buf = torch.empty(T_max, dtype=torch.float32, device=dev)
     ent_buf = torch.empty(T_max, dtype=torch.float32, device=dev)
 
+    dw_ready = torch.cuda.Event() if comm is not None and args.n2_overlap > 0 else None
+    n2_stream = torch.cuda.Stream() if dw_ready is not None else None
+
     def one_step(inputs):
         """inputs[i] = (device segment table, logp_old, logp_ref, rewards) of micro-batch i"""
         reps = []
@@ -383,12 +390,22 @@ def main():
             out = {"logp": logp_buf[:w.n_tokens], "entropy": ent_buf[:w.n_tokens],
                    "dhidden": dhidden_buf[:w.n_tokens], "dweight": dweight,
                    "report": mb["report"]}
+            last = i == len(mbs) - 1
+            overlap = comm is not None and args.n2_overlap > 0 and last
             res = step(packed, w.group_off, rw, mb["hidden"], weight, lo, lr,
                        norm_groups=n_groups_global, norm_tokens=norm_tokens, outputs=out,
-                       sync_report=False, accumulate_dweight=i > 0)
+                       sync_report=False, accumulate_dweight=i > 0,
+                       dw_ready=dw_ready if overlap else None,
+                       reserve_sms=args.n2_overlap if overlap else 0)
+            if overlap:  # N2 beside the last chunk's dH GEMM (tl_grpo_lmhead_step_overlap)
+                n2_stream.wait_event(dw_ready)
+                comm.allreduce_grad(dweight, stream=n2_stream)
             reps.append(res.report_tensor)
         rep = reps[0] if len(reps) == 1 else combine_reports_device(reps, agg)
-        if comm is not None:     # N1 + N2 at the C ABI (NCCL), stream-ordered
+        if comm is not None and args.n2_overlap > 0:
+            comm.allreduce_report(rep, agg)
+            torch.cuda.current_stream().wait_stream(n2_stream)
+        elif comm is not None:   # N1 + N2 at the C ABI (NCCL), stream-ordered
             comm.allreduce_report(rep, agg)
             comm.allreduce_grad(dweight)
         elif world > 1:          # gloo process group (ranks sharing one GPU)

@@ -292,6 +292,31 @@ int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight, const in
                         int32_t mode, void* workspace, size_t workspace_bytes,
                         tl_stream_t stream);
 
+/* N2 overlap (data parallel, see tl_allreduce_f32 below).  With
+ * dw_ready_event != NULL the step runs its last chunk's dW GEMM before that
+ * chunk's dH GEMM and records the event (a cudaEvent_t) on `stream` as soon
+ * as dweight is final; the last dH GEMM then leaves reserve_sms SMs free.  A
+ * caller that makes another stream wait on the event and issues the dW
+ * all-reduce / reduce-scatter there gets the collective running beside the
+ * last dH GEMM instead of after the step (every GEMM otherwise holds all
+ * SMs).  Outputs are bitwise those of tl_grpo_lmhead_step. */
+typedef struct tl_step_overlap {
+  void* dw_ready_event;  /* cudaEvent_t, or NULL */
+  int32_t reserve_sms;   /* >= 0; rounded up to whole CTA pairs */
+} tl_step_overlap;
+int tl_grpo_lmhead_step_overlap(const uint16_t* hidden, const uint16_t* weight,
+                                const int32_t* input_ids, const uint8_t* loss_mask,
+                                const int32_t* act_idx, int64_t n_act,
+                                const int32_t* traj_of_token, const int32_t* cu_seqlens,
+                                const int32_t* group_off, const float* logp_old,
+                                const float* logp_ref, const float* adv32, const float* traj_w,
+                                int64_t n_tokens, int32_t hidden_dim, int32_t vocab,
+                                int32_t n_traj, int32_t n_groups, const tl_loss_config* cfg,
+                                float* logp_out, float* entropy_out, uint16_t* dhidden,
+                                float* dweight, double* report, int32_t chunk_rows, int32_t mode,
+                                void* workspace, size_t workspace_bytes, tl_stream_t stream,
+                                const tl_step_overlap* overlap);
+
 /* ------------------------------------------------------------------------
  * F1 — episode-log / sidecar ingest (host, multithreaded C++).
  * Replaces rollout/episodes.read_episodes (episodes.py:132-147) +

@@ -43,7 +43,7 @@ EXPORTS = [
     "tl_loss_f32_workspace_bytes", "tl_loss_f32",
     "tl_lmhead_workspace_bytes", "tl_lmhead_logprobs_workspace_bytes",
     "tl_lmhead_step_workspace_bytes", "tl_lmhead_logprobs",
-    "tl_grpo_lmhead_step",
+    "tl_grpo_lmhead_step", "tl_grpo_lmhead_step_overlap",
     "tl_gemm_bf16",
     "tl_ingest_open", "tl_ingest_sizes", "tl_ingest_fill", "tl_ingest_free",
     "tl_tokenizer_create", "tl_tokenizer_free", "tl_tokenizer_vocab_size",
@@ -60,6 +60,10 @@ class LossConfigC(C.Structure):
         ("entropy_coef", C.c_double), ("use_mask", C.c_int32), ("has_ref", C.c_int32),
         ("objective", C.c_int32), ("agg", C.c_int32), ("entropy_norm", C.c_double),
     ]
+
+
+class StepOverlapC(C.Structure):
+    _fields_ = [("dw_ready_event", C.c_void_p), ("reserve_sms", C.c_int32)]
 
 
 class RewardParamsC(C.Structure):
@@ -104,6 +108,10 @@ _SIGS = {
     "tl_grpo_lmhead_step": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64,
                                       _I32, _I32, _I32, _I32, C.POINTER(LossConfigC), _P, _P, _P,
                                       _P, _P, _I32, _I32, _P, _SZ, _P]),
+    "tl_grpo_lmhead_step_overlap": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P,
+                                              _I64, _I32, _I32, _I32, _I32,
+                                              C.POINTER(LossConfigC), _P, _P, _P, _P, _P, _I32,
+                                              _I32, _P, _SZ, _P, C.POINTER(StepOverlapC)]),
     "tl_gemm_bf16": (C.c_int, [_P, _I32, _I64, _P, _I32, _I64, _I32, _I32, _I32, _P, _I32, _I64,
                                _I32, _P]),
     "tl_ingest_open": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),

@@ -123,7 +123,8 @@ constexpr int kMaxDevices = 64;
 
 template <int CG, bool A_MN, bool B_MN, class Epi, int BN = kBN>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s,
-                const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER) {
+                const typename Epi::Params& ep, cudaStream_t st, int prof_cat = PROF_GEMM_OTHER,
+                int reserve_sms = 0) {
   ProfScope prof(prof_cat, st);
   constexpr int kSt = BN <= 256 ? kStages : 4;  // 48 KB stages at BN = 512
   using Smem = GemmSmem<BN, kSt, CG>;
@@ -166,6 +167,9 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmShape& s
   }
   if (s.n_units == 0 || s.k_blocks == 0) return TL_OK;
   TL_REQUIRE(s.cg == CG, TL_ERR_INVALID_ARG, "shape built for cg=%d, kernel cg=%d", s.cg, CG);
+  // reserve_sms: leave whole CTA groups free for a concurrent kernel (a
+  // collective on another stream, tl_grpo_lmhead_step_overlap)
+  if (reserve_sms > 0) max_groups = max(1, max_groups - (reserve_sms + CG - 1) / CG);
   const int groups = s.n_units < max_groups ? s.n_units : max_groups;
   lc.gridDim = dim3(groups * CG);
   GemmShape sh = s;
@@ -523,9 +527,10 @@ constexpr int kDsOverlapCtasPerSm = 2;
 
 // Attach wave-lockstep counters to a shape (see GemmShape::sync_ctr) and
 // turn on the serpentine K order.
-GemmShape with_sync(GemmShape s, int* ctr, int every, int window, int split = 0) {
+GemmShape with_sync(GemmShape s, int* ctr, int every, int window, int split = 0,
+                    int reserve_sms = 0) {
   s.serpentine = 1;
-  const int n_pairs = num_sms() / s.cg;
+  const int n_pairs = max(1, num_sms() / s.cg - (reserve_sms + s.cg - 1) / s.cg);
   const int waves = (s.n_units + n_pairs - 1) / n_pairs;
   if (ctr && waves * (split ? 8 : 1) <= kSyncWaves && every > 0) {
     s.sync_ctr = ctr;
@@ -776,18 +781,20 @@ extern "C" int tl_lmhead_logprobs(const uint16_t* hidden, const uint16_t* weight
   return TL_OK;
 }
 
-extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight,
-                                   const int32_t* input_ids, const uint8_t* loss_mask,
-                                   const int32_t* act_idx, int64_t n_act,
-                                   const int32_t* traj_of_token, const int32_t* cu_seqlens,
-                                   const int32_t* group_off, const float* logp_old,
-                                   const float* logp_ref, const float* adv32, const float* traj_w,
-                                   int64_t n_tokens, int32_t H, int32_t V, int32_t n_traj,
-                                   int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
-                                   float* entropy_out, uint16_t* dhidden, float* dweight,
-                                   double* report, int32_t chunk_rows, int32_t mode_flags,
-                                   void* workspace, size_t workspace_bytes, tl_stream_t stream) {
+extern "C" int tl_grpo_lmhead_step_overlap(
+    const uint16_t* hidden, const uint16_t* weight, const int32_t* input_ids,
+    const uint8_t* loss_mask, const int32_t* act_idx, int64_t n_act, const int32_t* traj_of_token,
+    const int32_t* cu_seqlens, const int32_t* group_off, const float* logp_old,
+    const float* logp_ref, const float* adv32, const float* traj_w, int64_t n_tokens, int32_t H,
+    int32_t V, int32_t n_traj, int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
+    float* entropy_out, uint16_t* dhidden, float* dweight, double* report, int32_t chunk_rows,
+    int32_t mode_flags, void* workspace, size_t workspace_bytes, tl_stream_t stream,
+    const tl_step_overlap* overlap) {
   TL_REQUIRE(cfg, TL_ERR_INVALID_ARG, "cfg is NULL");
+  TL_REQUIRE(!overlap || overlap->reserve_sms >= 0, TL_ERR_INVALID_ARG, "reserve_sms < 0");
+  // N2 overlap: the last chunk runs dW before dH and announces the final dW
+  cudaEvent_t dw_ready = overlap ? static_cast<cudaEvent_t>(overlap->dw_ready_event) : nullptr;
+  const int reserve = overlap ? overlap->reserve_sms : 0;
   const int mode =
       mode_flags & ~(TL_LMHEAD_ACCUMULATE_DW | TL_LMHEAD_NO_SPLIT_TAIL | TL_LMHEAD_NO_FACTORED |
                      TL_LMHEAD_DEBUG_FIXUP);
@@ -924,8 +931,12 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
                            reinterpret_cast<__nv_bfloat16_raw*>(b.ds), Vld};
     return launch_gemm<kCG, false, false, EpiDSoftmax>(ma, mb, sh, ep, s_ds, PROF_GEMM_DS);
   };
-  // stage B: dH rows = dS W (scattered to packed positions), dW (+)= dS^T h_c
-  auto stage_bwd = [&](long long i) -> int {
+  // stage B: dH rows = dS W (scattered to packed positions), dW (+)= dS^T h_c.
+  // The last chunk with a dw_ready event: dW first, the event, then dH with
+  // `reserve` SMs left free, so the caller's dW collective (issued on another
+  // stream after the event) runs beside the dH GEMM.  Either order gives the
+  // same bits (dH does not read dW; each dH tile is one pair's full-K sum).
+  auto stage_dh = [&](long long i, int reserve_sms) -> int {
     const ChunkWs& b = *bufs[i & 1];
     const int rows = rows_of(i);
     const int32_t* ci = act_idx + i * chunk_rows;
@@ -940,14 +951,19 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       // (evict_last): -1.1 % dH (gpu_r50)
       const GemmShape sh = with_sync(
           make_shape(rows, H, V, kBNWide, 1, 1, kCG, tune::kDhPolA, tune::kDhPolB),
-          b.sync + 2 * kSyncWaves, tune::kBwdSyncBlocks, tune::kBwdSyncWindow);
+          b.sync + 2 * kSyncWaves, tune::kBwdSyncBlocks, tune::kBwdSyncWindow, 0, reserve_sms);
       // dhidden rows are written once and not read again in the step
       EpiStoreBF16::Params ep{reinterpret_cast<__nv_bfloat16_raw*>(dhidden), H, ci,
                               factored ? b.alpha : nullptr};
       if (int e = launch_gemm<kCG, false, true, EpiStoreBF16, kBNWide>(ma, mb, sh, ep, st,
-                                                                       PROF_GEMM_DH))
+                                                                       PROF_GEMM_DH, reserve_sms))
         return e;
     }
+    return TL_OK;
+  };
+  auto stage_dw = [&](long long i) -> int {
+    const ChunkWs& b = *bufs[i & 1];
+    const int rows = rows_of(i);
     if (!dweight) return TL_OK;
     CUtensorMap ma, mb;
     if (int e = make_ab_maps(&ma, &mb, b.ds, true, V, Vld, b.h, true, H, H, rows, kCG)) return e;
@@ -960,6 +976,15 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
     }
     EpiStoreF32::Params ep{dweight, H, (i > 0 || acc_dw) ? 1 : 0};
     return launch_gemm<kCG, true, true, EpiStoreF32, kBNWide>(ma, mb, sh, ep, st, PROF_GEMM_DW);
+  };
+  auto stage_bwd = [&](long long i) -> int {
+    if (dw_ready && i == n_chunks - 1) {
+      if (int e = stage_dw(i)) return e;
+      TL_CUDA_TRY(cudaEventRecord(dw_ready, st));
+      return stage_dh(i, reserve);
+    }
+    if (int e = stage_dh(i, 0)) return e;
+    return stage_dw(i);
   };
 
   if (!pipelined) {
@@ -990,6 +1015,26 @@ extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weigh
       if (int e = stage_bwd(i)) return e;
     }
   }
+  // no chunk (or no backward): dW is final now
+  if (dw_ready && (n_chunks == 0 || !bwd)) TL_CUDA_TRY(cudaEventRecord(dw_ready, st));
   return launch_reductions(c.term, c.k3o, c.flags, entropy_out, loss_mask, 1, cu_seqlens,
                            group_off, n_traj, n_groups, n_tokens, cfg->agg, c.red, report, st);
+}
+
+extern "C" int tl_grpo_lmhead_step(const uint16_t* hidden, const uint16_t* weight,
+                                   const int32_t* input_ids, const uint8_t* loss_mask,
+                                   const int32_t* act_idx, int64_t n_act,
+                                   const int32_t* traj_of_token, const int32_t* cu_seqlens,
+                                   const int32_t* group_off, const float* logp_old,
+                                   const float* logp_ref, const float* adv32, const float* traj_w,
+                                   int64_t n_tokens, int32_t H, int32_t V, int32_t n_traj,
+                                   int32_t n_groups, const tl_loss_config* cfg, float* logp_out,
+                                   float* entropy_out, uint16_t* dhidden, float* dweight,
+                                   double* report, int32_t chunk_rows, int32_t mode_flags,
+                                   void* workspace, size_t workspace_bytes, tl_stream_t stream) {
+  return tl_grpo_lmhead_step_overlap(hidden, weight, input_ids, loss_mask, act_idx, n_act,
+                                     traj_of_token, cu_seqlens, group_off, logp_old, logp_ref,
+                                     adv32, traj_w, n_tokens, H, V, n_traj, n_groups, cfg,
+                                     logp_out, entropy_out, dhidden, dweight, report, chunk_rows,
+                                     mode_flags, workspace, workspace_bytes, stream, nullptr);
 }

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 
 from . import _lib
@@ -240,20 +242,26 @@ class GRPOStep:
                  norm_tokens: float | None = None, stream=None, outputs=None,
                  adv_cache=None, sync_report: bool = True,
                  accumulate_dweight: bool = False, want_dhidden: bool = True,
-                 want_dweight: bool = True) -> StepResult:
+                 want_dweight: bool = True, dw_ready=None, reserve_sms: int = 0) -> StepResult:
         """One step over `packed`.  Micro-batching an optimizer step: call once
         per micro-batch with the step's global norm_groups / norm_tokens and
         accumulate_dweight=True after the first (outputs["dweight"] reused),
         then combine the reports with parallel.combine_reports.
         want_dweight=False: frozen LM head (dS + dH only, no dW GEMM);
         want_dhidden=False: dW only.  `stream`: a torch.cuda.Stream to run on
-        (temporaries are allocated in its order; the report read waits on it)."""
+        (temporaries are allocated in its order; the report read waits on it).
+        dw_ready: a torch.cuda.Event recorded as soon as dweight is final,
+        before the last chunk's dH GEMM, which then leaves reserve_sms SMs
+        free — make another stream wait on it and issue the dW all-reduce
+        there to overlap N2 with that GEMM (parallel.NcclComm.allreduce_grad;
+        include/toolloop_b200.h, tl_grpo_lmhead_step_overlap)."""
         with _on(stream):
             plan = self._prepare(packed, group_off, rewards, hidden, weight, logp_old, logp_ref,
                                  backward=backward, norm_groups=norm_groups,
                                  norm_tokens=norm_tokens, outputs=outputs, adv_cache=adv_cache,
                                  accumulate_dweight=accumulate_dweight,
-                                 want_dhidden=want_dhidden, want_dweight=want_dweight)
+                                 want_dhidden=want_dhidden, want_dweight=want_dweight,
+                                 dw_ready=dw_ready, reserve_sms=reserve_sms)
             if stream is not None:
                 plan.ws.record_stream(stream)
             self._launch(plan, stream)
@@ -286,7 +294,7 @@ class GRPOStep:
 
     def _prepare(self, packed, group_off, rewards, hidden, weight, logp_old, logp_ref, *,
                  backward, norm_groups, norm_tokens, outputs, adv_cache, accumulate_dweight,
-                 want_dhidden, want_dweight):
+                 want_dhidden, want_dweight, dw_ready=None, reserve_sms=0):
         import torch
 
         L = _lib.lib()
@@ -359,6 +367,14 @@ class GRPOStep:
                               entropy_norm=float(norm_tokens if norm_tokens is not None
                                                  else max(packed.n_act, 1)))
         plan.keep = (packed, hidden, weight, logp_old, logp_ref)  # pointers stay valid
+        plan.overlap = None
+        if dw_ready is not None:  # N2 overlap (tl_grpo_lmhead_step_overlap)
+            ev = dw_ready.cuda_event
+            if not ev:  # torch creates the CUDA event lazily, on its first record
+                dw_ready.record()
+                ev = dw_ready.cuda_event
+            plan.overlap = _lib.StepOverlapC(C.c_void_p(ev), int(reserve_sms))
+            plan.keep = plan.keep + (dw_ready,)
         plan.step_args = (
             hidden.data_ptr(), weight.data_ptr(), packed.input_ids.data_ptr(),
             packed.loss_mask.data_ptr(), packed.act_idx.data_ptr(), packed.n_act,
@@ -379,7 +395,10 @@ class GRPOStep:
         s = _lib.stream_handle(stream)
         if plan.adv_args is not None:
             _lib.check(L.tl_group_advantages(*plan.adv_args, s))
-        _lib.check(L.tl_grpo_lmhead_step(*plan.step_args, s))
+        if plan.overlap is not None:
+            _lib.check(L.tl_grpo_lmhead_step_overlap(*plan.step_args, s, C.byref(plan.overlap)))
+        else:
+            _lib.check(L.tl_grpo_lmhead_step(*plan.step_args, s))
 
 
 class _StepPlan:

@@ -215,3 +215,45 @@ def test_nccl_collectives_at_the_c_abi():
         assert d.tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("factored", [True, False])
+def test_n2_overlap_event_and_reserved_sms(factored):
+    """tl_grpo_lmhead_step_overlap: the last chunk runs dW before dH, records
+    dw_ready once dW is final and leaves SMs free for the dH GEMM's
+    neighbour; a dW all-reduce issued on a side stream after the event
+    (one-rank NCCL communicator: the identity) must see the final dW, and
+    every output equals the plain step bitwise."""
+    from paper_2509_01055_b200 import grpo, packing, parallel
+    from paper_2509_01055_b200.rl.loss import LossConfig
+    from paper_2509_01055_b200.trajectory import Segment, Trajectory
+
+    groups, lold, lref, hidden, W = _global_batch()
+    trajs = [Trajectory([Segment(o, "", x) for o, x in tr]) for g in groups for tr in g["trajs"]]
+    rewards = np.concatenate([g["rewards"] for g in groups])
+    go = np.arange(0, len(trajs) + 1, G, dtype=np.int32)
+    packed = packing.pack(trajs)
+    lo = torch.from_numpy(np.asarray(lold, dtype=np.float32)).cuda()
+    lr = torch.from_numpy(np.asarray(lref, dtype=np.float32)).cuda()
+    cfg = LossConfig(kl_beta=0.04, entropy_coef=0.0 if factored else 0.01)
+    step = grpo.GRPOStep(H, V, cfg, chunk_rows=CHUNK)  # several chunks
+    assert packed.n_act > 2 * CHUNK
+    ref = step(packed, go, rewards, hidden, W, lo, lr)
+    dh0, dw0 = ref.dhidden.clone(), ref.dweight.clone()
+    comm = parallel.NcclComm(parallel.NcclComm.unique_id(), 1, 0)
+    try:
+        ev, side = torch.cuda.Event(), torch.cuda.Stream()
+        res = step(packed, go, rewards, hidden, W, lo, lr, dw_ready=ev, reserve_sms=16)
+        side.wait_event(ev)
+        snap = torch.empty_like(res.dweight)
+        with torch.cuda.stream(side):
+            snap.copy_(res.dweight)               # what a collective after the event reads
+        comm.allreduce_grad(res.dweight, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        assert torch.equal(snap, dw0)
+        assert torch.equal(res.dweight, dw0) and torch.equal(res.dhidden, dh0)
+        assert res.report == ref.report
+        assert torch.equal(res.logp, ref.logp)
+    finally:
+        comm.close()
