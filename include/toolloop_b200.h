@@ -28,8 +28,10 @@
 extern "C" {
 #endif
 
-#define TL_ABI_VERSION 3  /* 2: tl_loss_config.entropy_norm, NCCL collectives
-                             3: tl_pack_varlen traj_drop, dW-only / dH-only steps */
+#define TL_ABI_VERSION 4  /* 2: tl_loss_config.entropy_norm, NCCL collectives
+                             3: tl_pack_varlen traj_drop, dW-only / dH-only steps
+                             4: factored store (TL_LMHEAD_NO_FACTORED / _DEBUG_FIXUP),
+                                tl_grpo_lmhead_step_overlap */
 
 typedef void* tl_stream_t; /* cudaStream_t */
 

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtoolloop_b200.so"
 if os.environ.get("TOOLLOOP_B200_LIB"):
     LIB_PATH = Path(os.environ["TOOLLOOP_B200_LIB"])
 
-TL_ABI_VERSION = 3  # include/toolloop_b200.h
+TL_ABI_VERSION = 4  # include/toolloop_b200.h
 TL_OK = 0
 TL_ERR_INVALID_ARG = 1
 TL_ERR_MASK_MISMATCH = 2

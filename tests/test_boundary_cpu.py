@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"missing export {s}"
     assert set(syms) == set(_lib.EXPORTS)
-    assert lib.tl_abi_version() == _lib.TL_ABI_VERSION == 3
+    assert lib.tl_abi_version() == _lib.TL_ABI_VERSION == 4
     assert lib.tl_launch_count() >= 0
 
 
