@@ -72,6 +72,33 @@ def test_pack_wide_segment_window_fallback():
     _check_pack(got, P.pack_varlen(trajs))
 
 
+@pytest.mark.parametrize("lead", [0, 1, 17])
+def test_pack_runs_of_empty_trajectories(lead):
+    """Hundreds of empty trajectories between (and after) short ones: a
+    16-segment tile in which > 256 trajectories start (the single-pass
+    packer's unstaged path), empty ones at tile starts, trailing empties."""
+    rng = np.random.default_rng(24 + lead)
+    trajs = [[("action", [1, 2, 3])] for _ in range(lead)]
+    for blk in range(6):
+        trajs += [[] for _ in range(300 + 7 * blk)]
+        trajs += _segments(rng, 40, (1, 5), (1, 12), empty_p=0.2, empty_traj_p=0.3)
+    trajs += [[] for _ in range(333)]
+    for drop in (None, rng.random(len(trajs)) < 0.3):
+        got = packing.pack([_traj(s) for s in trajs], drop=drop)
+        _check_pack(got, P.pack_varlen(trajs, drop=drop))
+
+
+def test_pack_long_trajectories_across_tiles():
+    """Trajectories of hundreds of segments (each spans many 16-segment
+    tiles: position ids restart only at trajectory starts)."""
+    rng = np.random.default_rng(29)
+    trajs = _segments(rng, 12, (150, 400), (0, 40), empty_p=0.15, empty_traj_p=0.0)
+    drop = rng.random(len(trajs)) < 0.25
+    for d in (None, drop):
+        got = packing.pack([_traj(s) for s in trajs], drop=d)
+        _check_pack(got, P.pack_varlen(trajs, drop=d))
+
+
 @pytest.mark.parametrize("shape", ["many_tiles", "c2_like"])
 def test_pack_drop(shape):
     rng = np.random.default_rng(23)
