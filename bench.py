@@ -319,7 +319,12 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
             # the step's own collectives (N1 report, N2 dW) go through the
             # library's NCCL communicator at the C ABI (tl_nccl_*)
-            comm = parallel.NcclComm.from_process_group()
+            try:
+                comm = parallel.NcclComm.from_process_group()
+            except Exception as e:  # keep the run: same collectives through torch's NCCL group
+                print(f"bench.py: NCCL at the C ABI unavailable ({e}); N1 / N2 via "
+                      "torch.distributed", file=sys.stderr)
+                comm = None
         else:
             dist.init_process_group(backend)
 
