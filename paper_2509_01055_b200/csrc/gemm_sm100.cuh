@@ -628,7 +628,12 @@ struct EpiStoreBF16 {
       if (!row_ok) return;
       const int cb = col0 + c;
       __nv_bfloat16_raw* dst = p.out + orow * p.ldo + cb;
-      auto val = [&](int j) { return scaled ? __uint_as_float(r[j]) * sc : __uint_as_float(r[j]); };
+      // a zero scale writes exact zeros whatever the accumulator holds (the
+      // factored backward's rows without gradient may sum far-off-anchor q
+      // past the fp32 range: 0 * inf must not become NaN)
+      auto val = [&](int j) {
+        return scaled ? (sc != 0.f ? __uint_as_float(r[j]) * sc : 0.f) : __uint_as_float(r[j]);
+      };
       if (cb + 32 <= s.N) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {

@@ -139,7 +139,9 @@ __device__ void combine_row(const CombineArgs& a, int r) {
     if (a.anchor) {
       const float d = lse - a.anchor[r];
       if (g == 0.f) {
-        a.alpha_row[r] = 0.f;  // no gradient: the row's q never matters
+        // no gradient: the row's q never matters (its dH row is written as
+        // exact zeros, its h_c row scales to zero; q itself stays finite)
+        a.alpha_row[r] = 0.f;
       } else if (d >= kQdMin && d <= kQdMax && !a.force_fixup) {
         a.alpha_row[r] = -g * expf(-d);
         // after every strip's q stores of this row (counter + fences)

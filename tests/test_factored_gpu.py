@@ -15,7 +15,9 @@ Checked here:
   * the out-of-range fallback (rows whose lse - m0 leaves [-45, 80] are
     recomputed on CUDA cores with m0 = lse): forced on every row
     (TL_LMHEAD_DEBUG_FIXUP), and reached naturally with |z| ~ 100 logits and
-    behaviour log-probs that are far from the current policy.
+    behaviour log-probs that are far from the current policy;
+  * far-off-anchor rows without a gradient (|z| ~ 150): exact-zero dH rows,
+    no NaN / inf.
 """
 
 import numpy as np
@@ -58,7 +60,7 @@ def _oracle_grads(trajs, rewards, go, packed, h, W, lold, lref, beta):
     lnew = np.zeros(T)
     lnew[act] = lp
     lo32 = lold.astype(np.float32).astype(np.float64)
-    lr32 = lref.astype(np.float32).astype(np.float64)
+    lr32 = None if lref is None else lref.astype(np.float32).astype(np.float64)
     ref, groups = _oracle_report(trajs, rewards, go, lnew, lo32, lr32, beta=beta)
     n_groups = len(go) - 1
     gl = np.zeros(T)
@@ -170,3 +172,30 @@ def test_entropy_bonus_keeps_fp16_store():
     _same_forward(a, b)
     assert torch.equal(a.dhidden, b.dhidden)
     assert torch.equal(a.dweight, b.dweight)
+
+
+def test_factored_far_rows_without_gradient_stay_finite():
+    """|z| ~ 150 logits, logp_old = 0 and no KL term: rows with logp_new
+    < -88 sit e^88+ above their anchor and have a zero gradient (clamped
+    ratio).  Their q saturates near the bf16 range and their dH accumulators
+    may overflow fp32; the zero row scale must still give exact-zero dH rows
+    and leave dW untouched (no NaN / inf anywhere)."""
+    H, V = 256, 1000
+    trajs, rewards, go, _, _, packed, h, W = _setup(H, V, seed=8, wstd=38.0 / 16.0)
+    from oracle import lmhead_oracle as LH
+
+    T = packed.n_tokens
+    act = packed.act_idx.cpu().numpy()
+    ids = packed.input_ids.cpu().numpy()
+    lp, _, _ = LH.lmhead_forward(_bf16_np(h)[act], _bf16_np(W), ids[act], exact=True)
+    assert (lp < -100).sum() >= 10, "the case must reach far-off-anchor rows"
+    lold = np.zeros(T)
+    cfg = L.LossConfig()
+    res = grpo.GRPOStep(H, V, cfg)(packed, go, rewards, h, W, _f(lold))
+    torch.cuda.synchronize()
+    assert torch.isfinite(res.dweight).all() and torch.isfinite(res.dhidden.float()).all()
+    far = act[lp < -30]  # ratio clamped (|logp_new - logp_old| > 20): zero gradient
+    assert torch.all(res.dhidden[torch.from_numpy(far).cuda()] == 0)
+    lp2, lse, ref, gl, dH, dW = _oracle_grads(trajs, rewards, go, packed, h, W, lold, None, 0.0)
+    tol = 1e-4 + 1e-5 * float(np.abs(lse).max())
+    _check_vs_oracle("factored_far_rows_no_grad", res, packed, lp2, ref, dH, dW, lp_tol=tol)

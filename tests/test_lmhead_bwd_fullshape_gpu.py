@@ -1,8 +1,8 @@
 """LM-head backward (dH / dW) parity at the benched shapes.
 
-The fused GRPO step at the C2 (H 3584, V 152064) and C5 (H 4096, V 151936)
-LM-head shapes, one whole synthetic group of the config (C2: ~17 k action
-rows, C5: ~40 k, so several chunks, 6 vocab strips, lockstep waves and the
+The fused GRPO step at the C1 (H 896, V 32000), C2 (H 3584, V 152064) and
+C5 (H 4096, V 151936) LM-head shapes, one whole synthetic group of the
+config (C1: ~2 k action rows; C2: ~17 k, C5: ~40 k, so several chunks, 6 vocab strips, lockstep waves and the
 dW split-K tail at its real size), against the float64 restatement
 `oracle.lmhead_oracle.lmhead_fwd_bwd_f64` on the same bf16 inputs.  The
 upstream per-token gradients come from the oracle's own forward (logp) and
@@ -91,7 +91,7 @@ def _case(shape, scale, seed=0):
 
 @pytest.mark.parametrize("mode", ["store", "factored", "recompute"])
 @pytest.mark.parametrize("scale", ["init", "realistic"])
-@pytest.mark.parametrize("shape", ["c2", "c5"])
+@pytest.mark.parametrize("shape", ["c1", "c2", "c5"])
 def test_backward_full_shape_vs_oracle(shape, scale, mode):
     cfg, wl, packed, h, W = _case(shape, scale)
     H, V = cfg.hidden, cfg.vocab
