@@ -41,7 +41,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "masked GRPO-step tokens/sec (pack+adv+logprob+loss) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "tokens/s"
 # ncu DRAM bytes of one C2 chunk (tools/profile_summary.py) for roofline.traffic
-TRAFFIC_JSON = "r2d_gemm_traffic.json"
+TRAFFIC_JSON = "r2f_gemm_traffic.json"
 
 
 def _peaks():
