@@ -2,14 +2,16 @@
 + surrogate loss + LM-head backward) on B200, vs the reference's CPU path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
-                    [--impl ours|reference] [--mode store|pipelined|recompute]
+                    [--impl ours|reference] [--mode store|store-fp16|pipelined|recompute]
+                    [--n2-overlap SMS]
 
 One step = the whole trajectory-to-loss hot path over one synthetic batch of
 BASELINE.json's config (default C2, Qwen2.5-7B shape: 256 prompts x 8
 rollouts, <= 4 tool turns, seq 4k, H 3584, V 152064, bf16):
   K1 pack (segment table -> varlen batch) -> K2 group advantages ->
-  K4 fused LM-head logp/entropy + GRPO surrogate epilogue (fp16 logits kept)
-  -> K5 backward (dS pass, dH = dS W, dW += dS^T H) -> deterministic
+  K4 fused LM-head logp/entropy + GRPO surrogate epilogue (keeps the chunk's
+  bf16 q = e^(z - m0): dS = alpha_r q without an entropy bonus)
+  -> K5 backward (dH = alpha (q W), dW += q^T (alpha H)) -> deterministic
   reductions [-> N1 report all-reduce, N2 dW all-reduce when N > 1].
 Configs whose activations exceed one GPU's HBM (C3, C4) run each step as
 micro-batches of whole groups with the step's global normalisers (dW

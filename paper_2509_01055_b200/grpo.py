@@ -179,8 +179,8 @@ class GRPOStep:
                  chunk_rows: int | None = None, recompute: bool = False,
                  pipelined: bool = False, split_tail: bool = True, factored: bool = True,
                  debug_fixup: bool = False):
-        """recompute=False keeps each chunk's logits in fp16 for the backward
-        (6*T*H*V FLOPs); True recomputes them in a second GEMM (8*T*H*V) so no
+        """recompute=False keeps each chunk's logits for the backward
+        (6*T*H*V FLOPs; bf16 q when factored, else fp16); True recomputes them in a second GEMM (8*T*H*V) so no
         logit ever leaves TMEM.  pipelined=True (store mode) double-buffers the
         chunk workspace and runs each chunk's dS pass beside the next chunk's
         forward GEMM (include/toolloop_b200.h, TL_LMHEAD_*); bitwise equal to
