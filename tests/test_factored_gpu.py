@@ -96,7 +96,7 @@ def _same_forward(a, b):
 
 
 @pytest.mark.parametrize("H,V,chunk", [(256, 1000, None), (128, 2304, 256), (192, 517, 128),
-                                       (128, 1000, 200)])
+                                       (128, 1000, 200), (64, 100, None), (64, 257, 64)])
 def test_factored_vs_fp16_store_and_oracle(H, V, chunk):
     trajs, rewards, go, lold, lref, packed, h, W = _setup(H, V)
     cfg = L.LossConfig(kl_beta=0.1)  # entropy_coef 0: the factored store applies
