@@ -8,7 +8,7 @@
 // index the LM head runs on.
 //
 //  pack_scan_kernel    single-pass decoupled look-back scan over the segment
-//                      table: 2,048 segments per CTA (tiles taken in order
+//                      table: 512 segments per CTA (tiles taken in order
 //                      from a ticket counter), exclusive prefix sums of the
 //                      (token, action-token) lengths -> packed offset and
 //                      action offset of every segment.
@@ -33,7 +33,7 @@ namespace tl {
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 2;  // 512-segment tiles: scan 9.7 -> 5.1 us at C2 vs 2,048 (gpu_s3n)
 constexpr int kScanTile = kScanThreads * kScanItems;  // segments per CTA
 
 // Look-back status word of a scan tile: flag (2 bits: 0 not ready,

@@ -56,11 +56,24 @@ def _segments(rng, n_traj, seg_range, len_range, empty_p=0.1, empty_traj_p=0.02,
 
 
 def test_pack_many_scan_tiles():
-    # ~40 k segments = 20 look-back tiles of 2,048 segments
+    # ~40 k segments = ~80 look-back tiles of 512 segments (look-back windows
+    # of 32 tiles: several rounds)
     rng = np.random.default_rng(21)
     trajs = _segments(rng, 3000, (1, 26), (1, 30))
     got = packing.pack([_traj(s) for s in trajs])
     _check_pack(got, P.pack_varlen(trajs))
+
+
+def test_pack_more_scan_tiles_than_sms():
+    # ~110 k segments = more look-back tiles than SMs: tiles are taken in
+    # ticket (dispatch) order instead of blockIdx order
+    rng = np.random.default_rng(28)
+    trajs = _segments(rng, 8500, (1, 26), (1, 4))
+    n_seg = sum(len(t) for t in trajs)
+    assert n_seg > 148 * 512
+    for drop in (None, rng.random(len(trajs)) < 0.1):
+        got = packing.pack([_traj(s) for s in trajs], drop=drop)
+        _check_pack(got, P.pack_varlen(trajs, drop=drop))
 
 
 def test_pack_wide_segment_window_fallback():
