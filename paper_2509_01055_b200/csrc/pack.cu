@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
-constexpr int kScatterThreads = 256;
-constexpr int kScatterRounds = 4;  // 8 rounds: scatter +9 %, 16: same (gpu_s3f)
+constexpr int kScatterThreads = 256;  // 128 x 8 rounds: same; 512 x 2: +28 % (gpu_s3o)
+constexpr int kScatterRounds = 4;  // 2: +9 %, 8: +9 %, 16: same (gpu_s3f, s3o)
 constexpr int kTilePos = kScatterThreads * 4 * kScatterRounds;  // packed positions per CTA
 constexpr int kSegCap = 1024;                                    // staged segments per CTA
 constexpr int kTrajCap = 512;                                    // staged trajectories per CTA
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kScatterThreads)
     }
     __syncthreads();
   }
-#pragma unroll 2
+#pragma unroll 2  // 4: +3 % (gpu_s3o)
   for (int r = 0; r < kScatterRounds; ++r) {
     const long long p0 = tile_begin + (static_cast<long long>(r) * kScatterThreads + threadIdx.x) * 4;
     if (p0 >= tile_end) break;
