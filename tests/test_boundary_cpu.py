@@ -97,3 +97,19 @@ def test_no_cpu_fallback():
 
     with pytest.raises(ExtensionMissing):
         group_advantages([1.0, 0.0])
+
+
+def test_struct_mirrors_match_the_header():
+    """ctypes mirrors of the header's structs: same field names, order and
+    size as the C declarations (tl_loss_config, tl_step_overlap)."""
+    import ctypes
+
+    from paper_2509_01055_b200 import _lib
+
+    text = (ROOT / "include" / "toolloop_b200.h").read_text()
+    for cname, py in (("tl_step_overlap", _lib.StepOverlapC), ("tl_loss_config", _lib.LossConfigC)):
+        body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (cname, cname), text, re.S).group(1)
+        fields = re.findall(r"\b(?:void\s*\*|double|int32_t|float)\s*\*?\s*(\w+)\s*;", body)
+        assert fields == [f for f, _ in py._fields_], cname
+    assert ctypes.sizeof(_lib.StepOverlapC) == 16
+    assert _lib.StepOverlapC.reserve_sms.offset == 8
