@@ -311,7 +311,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
+    # TL_BENCH_FORCE_PG=1 (tests): a one-rank process group and NCCL
+    # communicator, so the N1 / N2 collective path runs on a one-GPU box
+    use_pg = world > 1 or os.environ.get("TL_BENCH_FORCE_PG") == "1"
+    if use_pg:
         backend = os.environ.get("TL_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             # NCCL's init lines (nranks, NVLS / channels) go to stderr
@@ -415,7 +418,7 @@ def main():
         elif comm is not None:   # N1 + N2 at the C ABI (NCCL), stream-ordered
             comm.allreduce_report(rep, agg)
             comm.allreduce_grad(dweight)
-        elif world > 1:          # gloo process group (ranks sharing one GPU)
+        elif use_pg:            # gloo process group (ranks sharing one GPU)
             parallel.allreduce_report(rep, agg)
             parallel.allreduce_grad(dweight)
         return rep
@@ -424,7 +427,7 @@ def main():
         return [(mb["dtab"], mb["lold"], mb["lref"], mb["rewards"]) for mb in mbs]
 
     def barrier():
-        if world > 1:
+        if use_pg:
             dist.barrier()
 
     # ---- warm-up
@@ -448,12 +451,12 @@ def main():
     launches = _lib.launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
     t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
+    if use_pg:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
     rep = grpo.report_dict(rep_t.cpu())
     tok_global = torch.tensor([T, n_act], device=dev, dtype=torch.float64)
-    if world > 1:
+    if use_pg:
         dist.all_reduce(tok_global)
     T_all, A_all = (float(x) for x in tok_global.tolist())
     value = T_all / (ms / 1e3)
@@ -491,7 +494,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
-        if world > 1:
+        if use_pg:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": T_all / (float(ems.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(host_rep.numel() * 8),
@@ -502,7 +505,7 @@ def main():
     if rank != 0:
         if comm is not None:
             comm.close()
-        if world > 1:
+        if use_pg:
             dist.destroy_process_group()
         return
 
@@ -549,7 +552,7 @@ def main():
         "impl_config": {"action_tokens_per_s": A_all / (ms / 1e3),
                         "collectives": ("NCCL at the C ABI (tl_allreduce_report, tl_allreduce_f32)"
                                         if comm is not None else
-                                        ("torch.distributed " + dist.get_backend()) if world > 1
+                                        ("torch.distributed " + dist.get_backend()) if use_pg
                                         else "none"),
                         "chunk_rows": step.last_chunk, "micro_batches": len(mbs),
                         "lmhead_mode": args.mode + (
@@ -568,7 +571,7 @@ def main():
     print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if world > 1:
+    if use_pg:
         dist.destroy_process_group()
 
 

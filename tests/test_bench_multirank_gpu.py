@@ -64,3 +64,32 @@ def test_bench_rejects_world_mismatch():
     out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "tiny"], cwd=ROOT,
                          env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+@pytest.mark.parametrize("overlap", [0, 2])
+def test_one_rank_nccl_bench_path(overlap):
+    """The collective path the driver's N-GPU run takes — NCCL process group,
+    the library's NCCL communicator, N1 report / N2 dW at the C ABI, optional
+    N2 overlap with the last dH GEMM — on a one-rank group (every gpurun box
+    has one GPU), launched under torch.distributed.run like the driver."""
+    import socket
+
+    from paper_2509_01055_b200.synthetic import CONFIGS, group_act_tokens
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, TL_BENCH_FORCE_PG="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "1",
+           "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu",
+           "--n2-overlap", str(overlap)]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert "NCCL at the C ABI" in d["impl_config"]["collectives"]
+    cfg = CONFIGS["tiny"]
+    assert d["report"]["masked_tokens"] == int(np.sum(group_act_tokens(cfg, np.arange(cfg.prompts))))
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
