@@ -383,9 +383,6 @@ __device__ __forceinline__ uint4 dsoftmax8(uint4 q, int col0, float K, float A, 
 // through the non-coherent path so the warp's interleaved 16-byte requests
 // share L1 sectors) per step; the pass is HBM-bound and, at the power-capped
 // SM clock of the step, kept short in instructions.
-#ifndef TL_DS_VARIANT
-#define TL_DS_VARIANT 0
-#endif
 __global__ void __launch_bounds__(256)
     dsoftmax_inplace_kernel(uint4* __restrict__ buf, long long ld_vec,
                             const int16_t* __restrict__ zoff, long long ldo, int V, int rows,
@@ -394,62 +391,26 @@ __global__ void __launch_bounds__(256)
                             const float* __restrict__ ez) {
   const int nvec = (V + 7) / 8;
   const int nsl = (nvec + 3) / 4;
-#if TL_DS_VARIANT == 3
-  __shared__ float s_off[8192];
-#endif
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const float l2 = lse[r] * kLog2e, gg = g[r], cc = c[r];
     const float A = cc * ez[r] - gg, B = -cc, Bu = -cc * kLn2;
     const int yy = y[r];
     uint4* row = buf + static_cast<long long>(r) * ld_vec;
     const int16_t* off = zoff + static_cast<long long>(r) * ldo;
-#if TL_DS_VARIANT == 0 || TL_DS_VARIANT == 4
     for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x) {
       const float m = static_cast<float>(__ldg(off + sl)) * (1.f / 128.f);
       const float K = fmaf(m, kLog2e, -l2), Aw = fmaf(B, m, A);
       const int v0 = sl * 4;
       if (v0 + 4 <= nvec) {
         uint4 q[4];
-#if TL_DS_VARIANT == 0
 #pragma unroll
         for (int j = 0; j < 4; ++j) q[j] = __ldg(row + v0 + j);
-#else
-#pragma unroll
-        for (int j = 0; j < 4; ++j) q[j] = row[v0 + j];
-#endif
 #pragma unroll
         for (int j = 0; j < 4; ++j) row[v0 + j] = dsoftmax8(q[j], (v0 + j) * 8, K, Aw, Bu, yy, gg);
       } else {
         for (int v = v0; v < nvec; ++v) row[v] = dsoftmax8(row[v], v * 8, K, Aw, Bu, yy, gg);
       }
     }
-#elif TL_DS_VARIANT == 1 || TL_DS_VARIANT == 2 || TL_DS_VARIANT == 3
-#if TL_DS_VARIANT == 3
-    __syncthreads();
-    for (int sl = threadIdx.x; sl < nsl; sl += blockDim.x)
-      s_off[sl] = static_cast<float>(__ldg(off + sl)) * (1.f / 128.f);
-    __syncthreads();
-    auto word = [&](int v, uint4 q) {
-      const float m = s_off[v >> 2];
-      return dsoftmax8(q, v * 8, fmaf(m, kLog2e, -l2), fmaf(B, m, A), Bu, yy, gg);
-    };
-#else
-    auto word = [&](int v, uint4 q) {
-      const float m = static_cast<float>(__ldg(off + (v >> 2))) * (1.f / 128.f);
-      return dsoftmax8(q, v * 8, fmaf(m, kLog2e, -l2), fmaf(B, m, A), Bu, yy, gg);
-    };
-#endif
-    constexpr int kIn = TL_DS_VARIANT == 2 ? 4 : 2;
-    int v = threadIdx.x;
-    for (; v + (kIn - 1) * static_cast<int>(blockDim.x) < nvec; v += kIn * blockDim.x) {
-      uint4 q[kIn];
-#pragma unroll
-      for (int j = 0; j < kIn; ++j) q[j] = row[v + j * blockDim.x];
-#pragma unroll
-      for (int j = 0; j < kIn; ++j) row[v + j * blockDim.x] = word(v + j * blockDim.x, q[j]);
-    }
-    for (; v < nvec; v += blockDim.x) row[v] = word(v, row[v]);
-#endif
   }
 }
 

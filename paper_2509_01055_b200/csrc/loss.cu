@@ -574,11 +574,7 @@ int launch_units(UnitArgs a, long long n_tokens, cudaStream_t st) {
   a.vec_ok = al(a.mask, 4) && al(a.lnew, 16) && al(a.lold, 16) && al(a.lref, 16) && al(a.grad, 16) &&
              al(a.term, 16) && al(a.k3o, 16) && al(a.flags, 4) && al(a.ent, 16);  // NULL is aligned
   a.n_slots = unit_slots(n_tokens, a.n_traj);
-#ifndef TL_K3_SLOTS_PER_CTA
-#define TL_K3_SLOTS_PER_CTA 0
-#endif
-  long long ctas = static_cast<long long>(num_sms()) * kUnitCtasPerSm;
-  if (TL_K3_SLOTS_PER_CTA > 0) ctas = (a.n_slots + TL_K3_SLOTS_PER_CTA - 1) / TL_K3_SLOTS_PER_CTA;
+  const long long ctas = static_cast<long long>(num_sms()) * kUnitCtasPerSm;
   const unsigned grid = static_cast<unsigned>(a.n_slots < ctas ? a.n_slots : ctas);
   if constexpr (kCompute) {  // the config's reference / objective choices as template flags
     const int v = (a.cfg.has_ref ? 1 : 0) | (a.cfg.objective ? 2 : 0);
