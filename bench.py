@@ -59,7 +59,7 @@ def _peaks():
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -91,7 +91,7 @@ class ClockSampler:
         self.f.flush()
         rows = [l.split(",") for l in Path(self.f.name).read_text().splitlines() if l.strip()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, lim, reasons = [], [], [], [], set()
         for r in rows:
             try:
                 sm.append(float(r[0]))
@@ -101,9 +101,18 @@ class ClockSampler:
             for n, v in zip(names, r[2:6]):
                 if "Active" in v and "Not" not in v:
                     reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(max(mx)) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+            try:  # board power (W): the step runs at the power limit
+                pw.append(float(r[6]))
+                lim.append(float(r[7]))
+            except (IndexError, ValueError):
+                pass
+        out = {"sm_mhz": float(np.median(sm)) if sm else None,
+               "sm_max_mhz": float(max(mx)) if mx else None,
+               "samples": len(sm), "reasons": sorted(reasons)}
+        if pw:
+            out["power_w"] = float(np.median(pw))
+            out["power_limit_w"] = float(max(lim))
+        return out
 
 
 # ---------------------------------------------------------- CPU baseline --
